@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Benchmark of the field-mapping hot path (BASELINE.json metric).
+
+Workload (default, `--config c2`): BASELINE.json configs[1] -- XGC-like graded
+poloidal-plane disk, disk_graded(1, 577, 0.6) = 1,000,519 source vertices ->
+DEGAS2-like uniform disk(1, 577) = 1,000,519 targets, MLS degree 2, C4
+("Wendland") weights a=2, AdaptiveRadius(12, h_src, 1.5), 8-component field
+f_c = sin((c+1)x) cos(y) + 2.  Synthetic inputs (synth.py restates the
+reference generators bit for bit).
+
+One step = the whole hot path over that batch, inputs resident in HBM:
+  source binning (grid build) -> target ordering -> adaptive radius count
+  -> CSR scan -> fused fill + C4 weights + QR fit (operator build)
+  -> 8-component operator apply   [-> NCCL all-gather of the target field, N>1]
+value = targets mapped per second (whole job).  `e2e` = the same through the
+public API (PreparedTransfer(...).apply(...)) with host inputs: H2D of
+sources/targets/field and D2H of the result inside the timed region.
+
+N>1 (torchrun): weak scaling -- every rank maps its own 1,000,519 targets
+(the target disk rotated by a rank-dependent angle) against the replicated
+source cloud, then the full target field is all-gathered to every rank.
+
+`--impl reference`: the reference's own CPU kernels (oracle/_ref = the
+reference's _ext.pyx compiled here) on all host cores, on a bounded sample.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "target points mapped/sec (search+MLS build, apply GB/s) at 1/2/4/8 B200 vs CPU"
+C2_H = 0.001956233500370731  # synth.disk_graded(1, 577, 0.6).mean_edge_length (pinned in tests)
+C1_H = 0.011486339741053897  # synth.square(99).mean_edge_length
+
+
+# ---------------------------------------------------------------- inputs
+def workload(config, rank=0):
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200 import synth
+
+    if config == "c2":
+        src = synth.disk_graded(1.0, 577, 0.6).coords
+        tgt = synth.disk(1.0, 577).coords
+        if rank:
+            a = 0.1 * rank  # weak scaling: a distinct target set per rank
+            c, s = math.cos(a), math.sin(a)
+            tgt = np.ascontiguousarray(tgt @ np.array([[c, s], [-s, c]]))
+        X = synth.sincos_field(src, 8)
+        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
+                         P.AdaptiveRadius(12, C2_H, 1.5))
+        desc = {"workload": "C2: disk_graded(1,577,0.6) 1,000,519 sources -> disk(1,577) "
+                            "1,000,519 targets per GPU, MLS degree 2, C4 (Wendland) a=2, "
+                            "AdaptiveRadius(12, h_src, 1.5), 8-component field",
+                "sources": int(src.shape[0]), "targets_per_gpu": int(tgt.shape[0]),
+                "components": 8, "degree": 2, "rbf": "c4", "selection": "adaptive(12,h,1.5)"}
+    elif config == "c1":
+        src = synth.square(99).coords
+        tgt = np.random.RandomState(rank).uniform(0, 1, (10000, 2))
+        X = synth.sincos_field(src, 1)
+        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.FixedRadius(2 * C1_H))
+        desc = {"workload": "C1: square(99) 10,000 sources -> 10,000 random targets, MLS "
+                            "degree 2, C4 a=2, FixedRadius(2h), scalar",
+                "sources": 10000, "targets_per_gpu": 10000, "components": 1, "degree": 2,
+                "rbf": "c4", "selection": "fixed(2h)"}
+    else:
+        raise SystemExit(f"unknown config {config}")
+    return src, tgt, X, spec, desc
+
+
+# --------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def fit_flops(counts, k):
+    """F(m,k) = 2mk^2 - (2/3)k^3 + 6mk + k^2 + m per target."""
+    m = counts.astype(np.float64)
+    return float(np.sum(2 * m * k * k - (2.0 / 3.0) * k ** 3 + 6 * m * k + k * k + m))
+
+
+# ------------------------------------------------------------ b200 arm
+# kernels launched by one device step (our own, counted from the launch
+# sequence in device.py / libfieldmap.so): source bbox 3, grid build 7,
+# target order 5, r_max bboxes 6, count 2, scan 3, operator build 2, apply 1
+LAUNCHES_PER_STEP = 3 + 7 + 5 + 6 + 2 + 3 + 2 + 1
+
+
+def b200_step(src_d, tgt_d, X_d, spec, marks):
+    import torch
+
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200.pointwise import _r_max_device
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((name, e))
+
+    mark("start")
+    cloud = D.SourceCloud(src_d)
+    mark("grid")
+    perm = cloud.target_order(tgt_d)
+    mark("order")
+    sel = spec.selection
+    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, _r_max_device(cloud.pts, tgt_d)) \
+        if hasattr(sel, "min_points") else D.fixed(sel.r_c)
+    cnt = D.count_supports(cloud, tgt_d, dsel, perm, 0)
+    mark("count")
+    op, stats = D.build_operator(cloud, tgt_d, dsel, cnt, P._rbf_pair(spec.rbf), spec.degree,
+                                 spec.lam, spec.centering, perm)
+    mark("build")
+    Y = op.apply(X_d)
+    mark("apply")
+    return Y, op, cnt, stats
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200.distributed import gather_target_field
+
+    torch.cuda.set_device(local_rank)
+    src, tgt, X, spec, desc = workload(args.config, rank)
+    nt_local = tgt.shape[0]
+    src_d, tgt_d, X_d = D.to_device(src), D.to_device(tgt), D.to_device(X)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step(marks):
+        Y, op, cnt, stats = b200_step(src_d, tgt_d, X_d, spec, marks)
+        if world > 1:
+            Y = gather_target_field(Y, nt_local * world)
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append(("allgather", e))
+        return Y, op, cnt, stats
+
+    for _ in range(args.warmup):
+        Y, op, cnt, stats = step([])
+    torch.cuda.synchronize()
+    if int(stats[0].item()) != 0:
+        raise SystemExit(f"{int(stats[0].item())} fits failed in the benchmark workload")
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    phase = {}
+    step_ms = []
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the step events)
+            marks = []
+            Y, op, cnt, stats = step(marks)
+            torch.cuda.synchronize()
+            for (a, ea), (b, eb) in zip(marks[:-1], marks[1:]):
+                phase[b] = phase.get(b, 0.0) + ea.elapsed_time(eb)
+            step_ms.append(marks[0][1].elapsed_time(marks[-1][1]))
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = nt_local * world * args.steps / (total_ms * 1e-3)
+
+    # roofline inputs (per launch, from this run's own CUDA events)
+    counts = cnt.counts.cpu().numpy()
+    k = P.n_monomials(spec.degree, 2)
+    flops = fit_flops(counts, k)
+    build_ms = phase["build"] / args.steps
+    apply_ms = phase["apply"] / args.steps
+    C = X.shape[1]
+    apply_bytes = op.algorithmic_bytes(C)
+    peaks = measured_peaks()
+    fp64_peak = D.fp64_probe() if rank == 0 else None
+
+    # e2e through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        src_h = torch.from_numpy(src).pin_memory()
+        tgt_h = torch.from_numpy(tgt).pin_memory()
+        X_h = torch.from_numpy(X).pin_memory()
+        for _ in range(max(1, args.warmup // 2)):
+            P.PreparedTransfer(src_h, tgt_h, spec).apply(X_h)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            Yh = P.PreparedTransfer(src_h, tgt_h, spec).apply(X_h)
+            if world > 1:
+                Yh = gather_target_field(Yh, nt_local * world).cpu()
+            Yh = Yh.cpu().numpy() if isinstance(Yh, torch.Tensor) else Yh
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": nt_local * world * args.steps / e2e_s, "unit": "targets/s",
+               "h2d_bytes_per_step": int(src.nbytes + tgt.nbytes + X.nbytes),
+               "d2h_bytes_per_step": int(nt_local * world * C * 8),
+               "ms_per_step": 1e3 * e2e_s / args.steps}
+
+    if rank != 0:
+        return None
+    cpu = None if (args.no_cpu or world > 1) else cpu_baseline(args, src, tgt, X, spec)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "targets/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference mesh generators restated bitwise; fields sin((c+1)x)cos(y)+2)",
+        "config": dict(desc, parallelism=f"target-sharded x{world}" + (
+            " + NCCL all-gather of the target field" if world > 1 else ""),
+            l2="flushed between timed steps (256 MiB write)"),
+        "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "roofline": {
+            "kernel": "k_fused_fit (fused fill + C4 weights + Householder QR + operator row)",
+            "bound": "fp64",
+            "achieved": flops / (build_ms * 1e-3) / 1e12,
+            "peak": fp64_peak,
+            "unit": "TFLOP/s",
+            "frac": (flops / (build_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
+            "traffic": None,
+            "note": "algorithmic FP64 flops F(m,k) summed over this step's supports; peak = "
+                    "DFMA-chain probe measured in this run (MEASURED_PEAKS.json has no FP64 "
+                    "figure); the build is issue/latency bound, not FP64 bound",
+        },
+        "roofline_apply": {
+            "kernel": "k_apply (CSR SpMM, 8 components)",
+            "bound": "hbm",
+            "achieved": apply_bytes / (apply_ms * 1e-3) / 1e9,
+            "peak": peaks.get("hbm_gbs"),
+            "unit": "GB/s",
+            "frac": apply_bytes / (apply_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+            "traffic": None,
+            "algorithmic_bytes": apply_bytes,
+            "note": "bytes = nnz*12 + nt*4 + ns*C*8 + nt*C*8 (SURVEY §8(d)); peak of measured"
+                    if not peaks.get("fallback") else "peak of fallback",
+        },
+        "nnz": op.nnz,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": sampler.summary(),
+    }
+    return line
+
+
+# ------------------------------------------------------- reference arm
+_REF = {}  # state shared with forked workers (set before the fork, never pickled)
+
+
+def _ref_chunk(bounds):
+    """Worker: the reference's compiled kernels on one target chunk."""
+    b0, b1 = bounds
+    st = _REF
+    from oracle import ref
+
+    E = ref.ext()
+    g, spec, X, src = st["grid"], st["spec"], st["X"], st["src"]
+    sel = spec.selection
+    tg = st["tg"][b0:b1]
+    off, idx, dist, radii, status = E.adaptive_radius_supports(
+        tg, g.points, float(g.lo[0]), float(g.lo[1]), g.dx, g.dy, g.nx, g.ny, g.cell_offsets,
+        g.cell_items, sel.min_points, sel.r0, sel.growth, st["r_max"])
+    w = np.empty(idx.shape[0])
+    for i in range(tg.shape[0]):  # pointwise.py:266-269 (per-target weight loop)
+        w[off[i]:off[i + 1]] = E.rbf_weights(st["kind"], spec.rbf.a, float(radii[i]),
+                                             dist[off[i]:off[i + 1]])
+    w = np.abs(w)  # pointwise.py:301
+    out = np.empty((tg.shape[0], X.shape[1]))
+    for c in range(X.shape[1]):  # PreparedTransfer.apply re-solves per component
+        v, _c, _st = E.fit_many(tg, off, idx, w, src, st["Xc"][c], spec.degree, spec.lam,
+                                spec.centering)
+        out[:, c] = v
+    return out
+
+
+def reference_sample(src, tgt, X, spec, nsample, procs):
+    """Time the reference CPU path on `nsample` targets with `procs` processes:
+    PointGrid build (restated, oracle/pointgrid.py) + the reference's compiled
+    adaptive_radius_supports / rbf_weights / fit_many (oracle/_ref) per chunk."""
+    import multiprocessing as mp
+
+    from oracle.oracle import r_max_for
+    from oracle.pointgrid import OraclePointGrid
+    from paper_2510_18838_b200.pointwise import _KIND_CODE
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    t0 = time.perf_counter()
+    _REF.update(grid=OraclePointGrid(src), r_max=r_max_for(src, tgt), spec=spec, X=X, src=src,
+                tg=np.ascontiguousarray(tgt[:nsample]), kind=_KIND_CODE[spec.rbf.kind],
+                Xc=[np.ascontiguousarray(X[:, c]) for c in range(X.shape[1])])
+    bounds = np.linspace(0, nsample, procs + 1).astype(int)
+    work = [(int(b0), int(b1)) for b0, b1 in zip(bounds[:-1], bounds[1:])]
+    if procs > 1:
+        with mp.get_context("fork").Pool(procs) as pool:
+            parts = pool.map(_ref_chunk, work)
+    else:
+        parts = [_ref_chunk(w) for w in work]
+    dt = time.perf_counter() - t0
+    return np.concatenate(parts), dt
+
+
+def cpu_baseline(args, src, tgt, X, spec, procs=None):
+    from oracle import ref
+
+    if not ref.available():
+        return {"unavailable": "oracle/_ref not built"}
+    procs = procs or (os.cpu_count() or 1)
+    nsample = min(tgt.shape[0], 2000 * procs)
+    _, dt = reference_sample(src, tgt, X, spec, nsample, procs)
+    return {"value": nsample / dt, "unit": "targets/s", "cores": procs, "kind": "reference",
+            "sample": f"first {nsample} targets of the workload, all {X.shape[1]} components, "
+                      f"{procs} processes; PointGrid of all sources rebuilt per run"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    src, tgt, X, spec, desc = workload(args.config, 0)
+    procs = os.cpu_count() or 1
+    nsample = min(tgt.shape[0], 2000 * procs)
+    for _ in range(args.warmup):
+        reference_sample(src, tgt, X, spec, min(nsample, 4 * procs), procs)
+    total = 0.0
+    for _ in range(args.steps):
+        _, dt = reference_sample(src, tgt, X, spec, nsample, procs)
+        total += dt
+    value = nsample * args.steps / total
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "targets/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(desc, parallelism=f"{procs} host processes"),
+        "cpu_baseline": {"value": value, "unit": "targets/s", "cores": procs,
+                         "kind": "reference",
+                         "sample": f"first {nsample} targets of the workload per step"},
+        "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=["c1", "c2"], default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_b200(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/*
+ * fieldmap.h -- C ABI of the B200 field-mapping library (libfieldmap.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `fieldbridge`
+ * (/root/reference/pkg/src/fieldbridge).  The reference's kernel seam is the
+ * module `fieldbridge._kernels` (_kernels/__init__.py:9-42), which binds
+ * either the Cython extension (_kernels/_ext.pyx) or the numpy fallback
+ * (_kernels/_pure.py).  Every entry point below replaces one function of
+ * that seam (or the Python code directly around it) and cites it.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (CUDA global memory) unless the
+ *     parameter name ends in `_host`.  Struct arguments are host pointers to
+ *     plain-old-data descriptors.
+ *   - Every call is enqueued on `stream` and returns immediately; outputs are
+ *     valid once the stream reaches that point.  No call allocates device
+ *     memory: scratch is caller-owned, sized by the matching *_workspace()
+ *     query.
+ *   - Return value: FM_OK (0) or a negative FM_ERR_* code.  Numerical
+ *     failures are never errors: they are reported per target in `status`
+ *     arrays exactly like the reference (FIT_OK/SINGULAR/EMPTY, _ext.pyx:27-29;
+ *     adaptive status, _ext.pyx:266).
+ *   - Reentrant: no global mutable state; calls on different streams may
+ *     overlap.
+ *   - Layouts: points are row-major (n, dim) fp64; fields are row-major
+ *     (n, ncomp) fp64 (component c of point p at p*ncomp + c).
+ */
+#ifndef FIELDMAP_H
+#define FIELDMAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *fm_stream_t; /* == cudaStream_t */
+
+#define FM_OK 0
+#define FM_ERR_ARG (-1)         /* invalid argument / shape */
+#define FM_ERR_CUDA (-2)        /* a CUDA launch or runtime call failed */
+#define FM_ERR_UNSUPPORTED (-3) /* dimension / degree / size not compiled */
+#define FM_ERR_WORKSPACE (-4)   /* caller scratch too small */
+
+#define FM_MAX_DIM 5
+
+/* RBF kind codes: identical to _ext.pyx:18-25 / _pure.py:13-20. */
+#define FM_RBF_GAUSSIAN 0
+#define FM_RBF_C4 1
+#define FM_RBF_CONST 2
+#define FM_RBF_IDENTITY 3
+#define FM_RBF_MULTIQUADRIC 4
+#define FM_RBF_INVERSE_MULTIQUADRIC 5
+#define FM_RBF_THIN_PLATE_SPLINE 6
+#define FM_RBF_CUBIC_SPLINE 7
+
+/* fit status codes: _ext.pyx:27-29. */
+#define FM_FIT_OK 0
+#define FM_FIT_SINGULAR 1
+#define FM_FIT_EMPTY 2
+
+/* Uniform bucket grid over the source cloud (locate.py:65-99, 144-161).
+ * A point's cell along axis a is clamp(trunc((v - lo[a]) * inv_d[a]), 0,
+ * n[a]-1) (_ext.pyx:78-85); cells are linearised with axis 0 fastest
+ * (the reference's `iy * nx + ix`, _ext.pyx:189). */
+typedef struct fm_grid {
+    int32_t dim;
+    int32_t reserved;
+    int64_t n[FM_MAX_DIM];
+    double lo[FM_MAX_DIM];
+    double inv_d[FM_MAX_DIM];
+    int64_t ncell;
+} fm_grid;
+
+/* Support selection (pointwise.py:94-119): fixed radius (r_c) or adaptive
+ * radius (min_pts, r0, growth, r_max with r_max from pointwise.py:253-255). */
+typedef struct fm_select {
+    int32_t adaptive;
+    int32_t min_pts;
+    double r_c;
+    double r0;
+    double growth;
+    double r_max;
+} fm_select;
+
+/* Radial weight (pointwise.py:75-91): kind code and shape parameter a; the
+ * cutoff is the selection radius (fixed: r_c, pointwise.py:250; adaptive:
+ * the per-target final radius, pointwise.py:266-269).  The |w| of
+ * _fit_batch (pointwise.py:301) is applied where weights feed a fit. */
+typedef struct fm_rbf {
+    int32_t kind;
+    int32_t reserved;
+    double a;
+} fm_rbf;
+
+/* Local polynomial fit (pointwise.py:134-161; _ext.pyx:291-293).  degree
+ * 0..3, dim 1..5 with n_monomials(dim, degree) <= 21. */
+typedef struct fm_fit {
+    int32_t dim;
+    int32_t degree;
+    double lam;
+    int32_t centering;
+    int32_t reserved;
+} fm_fit;
+
+/* ------------------------------------------------------------------ info */
+int fm_version(void);
+const char *fm_error_string(int code);
+/* n_monomials (pointwise.py:70-72, generalised to `dim` axes). */
+int fm_n_monomials(int dim, int degree);
+
+/* --------------------------------------------------- a1: source binning
+ * Replaces PointGrid/_CsrGrid construction (locate.py:144-161, 65-87):
+ * counting (radix) sort of the sources by cell key.  Outputs the CSR
+ * cell_start[ncell+1] and the sources in cell order (ids ascending inside a
+ * cell) as sorted_ids[n] / sorted_pts[n*dim]. */
+size_t fm_grid_workspace(int64_t n, int64_t ncell);
+int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *cell_start,
+                  int32_t *sorted_ids, double *sorted_pts, void *workspace,
+                  size_t workspace_bytes, fm_stream_t stream);
+
+/* Bounding box of n points: lohi[0..dim) = min, lohi[dim..2dim) = max
+ * (device).  The `bbox` of locate.py:151. */
+int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t stream);
+
+/* Processing order of targets (cell order of the source grid) for locality.
+ * Results never depend on it; perm[k] = target processed k-th. */
+size_t fm_order_workspace(int64_t nt, int64_t ncell);
+int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
+                    void *workspace, size_t workspace_bytes, fm_stream_t stream);
+
+/* --------------------------------------------- a3/a4: radius search
+ * Count pass of fixed_radius_supports (_ext.pyx:215-220) and the radius
+ * growth loop of adaptive_radius_supports (_ext.pyx:256-272).  counts[t] is
+ * the number of sources with fl(sqrt(sum dx^2)) < r (strict).  For adaptive
+ * selection radii[t] / status[t] are the reference's `radii` / `status`
+ * (status 1: r_max reached with fewer than min_pts sources); radii/status may
+ * be NULL for a fixed radius.  perm may be NULL (identity order).
+ * stats (device int32[6], may be NULL; written by the call) receives
+ *   [0] max count  [1] min count
+ *   [2] #targets with count < min_required  [3] first such target (INT32_MAX if none)
+ *   [4] #targets with status != 0           [5] first such target
+ * which is what pointwise.py:243-249 / 260-265 need to raise
+ * UnderdeterminedError / InsufficientSourcesError naming the first target. */
+int fm_support_count(const fm_grid *grid, const int32_t *cell_start,
+                     const double *sorted_pts, const double *targets, int64_t nt,
+                     const int32_t *perm, const fm_select *sel, int32_t min_required,
+                     int32_t *counts, double *radii, uint8_t *status, int32_t *stats,
+                     fm_stream_t stream);
+
+/* offsets[0] = 0, offsets[i+1] = offsets[i] + counts[i] (np.cumsum of
+ * _ext.pyx:220/272). */
+size_t fm_scan_workspace(int64_t n);
+int fm_offsets_from_counts(const int32_t *counts, int64_t n, int64_t *offsets,
+                           void *workspace, size_t workspace_bytes, fm_stream_t stream);
+
+/* Fill pass (_ext.pyx:225-234, 277-287): per target the source ids with
+ * d < r in ascending id order, and d, written at offsets[t].  When rbf and
+ * w are non-NULL also writes the raw radial weights (rbf_weights at the
+ * selection radius; pointwise.py:250, 266-269), fused.  max_count must be
+ * >= every counts[t] (as returned by fm_support_count). */
+int fm_support_fill(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+                    const int32_t *sorted_ids, const double *targets, int64_t nt,
+                    const int32_t *perm, const fm_select *sel, const double *radii,
+                    const int64_t *offsets, int32_t max_count, int64_t *idx, double *dist,
+                    const fm_rbf *rbf, double *w, fm_stream_t stream);
+
+/* ------------------------------------------------- a5: radial weights
+ * rbf_weights(kind, a, r_c, r) (_ext.pyx:65-75). */
+int fm_rbf_weights(int kind, double a, double r_c, const double *r, int64_t n, double *out,
+                   fm_stream_t stream);
+
+/* ------------------------------------------------------ a7: fit_many
+ * fit_many (_ext.pyx:291-426) on caller-supplied supports: values[nt]
+ * (NaN on failure), coeffs[nt*k] (NaN rows), status[nt].  sup_w are the
+ * weights as passed to the reference's fit_many (already |w|).  src_val is
+ * (ns,) -- one component.  max_m >= every support size.
+ * stats (device int32[2], may be NULL; written by the call): [0] #targets
+ * with status != FIT_OK, [1] first such target (INT32_MAX if none) --
+ * pointwise.py:305-313 raises SingularFitError on the first one. */
+int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int64_t *sup_off,
+                const int64_t *sup_idx, const double *sup_w, int32_t max_m, const double *src,
+                const double *src_val, double *values, double *coeffs, uint8_t *status,
+                int32_t *stats, fm_stream_t stream);
+
+/* --------------------------------- a8/a13: transfer operator (new)
+ * Fused fill + weights + fit producing the explicit transfer operator
+ * W (nt x ns, CSR rows at offsets, ids ascending): row t holds
+ * W[t, j] = e_t^T (the value functional of the reference's fit) so that
+ * W @ f reproduces fit_many's `values` for every field f (the fit is linear
+ * in src_val, _ext.pyx:394).  col[nnz] = source id, val[nnz] = weight
+ * (NaN row on failure), status[nt] and stats[2] as fit_many.  This is what
+ * PreparedTransfer (pointwise.py:399-431) caches instead of the raw support. */
+int fm_build_operator(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+                      const int32_t *sorted_ids, const double *targets, int64_t nt,
+                      const int32_t *perm, const fm_select *sel, const double *radii,
+                      const int64_t *offsets, int32_t max_count, const fm_rbf *rbf,
+                      const fm_fit *fit, const double *src, int32_t *col, double *val,
+                      uint8_t *status, int32_t *stats, fm_stream_t stream);
+
+/* One-shot fused transfer of a scalar field (fit_point_cloud,
+ * pointwise.py:434-451): fill + weights + fit_many per target without
+ * materialising supports.  values[nt] (NaN on failure), status[nt],
+ * stats[2] as fit_many. */
+int fm_transfer_values(const fm_grid *grid, const int32_t *cell_start,
+                       const double *sorted_pts, const int32_t *sorted_ids,
+                       const double *targets, int64_t nt, const int32_t *perm,
+                       const fm_select *sel, const double *radii, int32_t max_count,
+                       const fm_rbf *rbf, const fm_fit *fit, const double *src,
+                       const double *src_val, double *values, uint8_t *status,
+                       int32_t *stats, fm_stream_t stream);
+
+/* Apply the operator to a multi-component field: Y[t, :] = sum_j
+ * val[j] * X[col[j], :] over row t (PreparedTransfer.apply,
+ * pointwise.py:418-431, without re-solving).  X (ns, ncomp), Y (nt, ncomp)
+ * row-major.  row_order (may be NULL) is the processing order (perm). */
+int fm_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const double *val,
+             const int32_t *row_order, const double *X, int32_t ncomp, double *Y,
+             fm_stream_t stream);
+
+/* ---------------------------------------------------- measurement
+ * FP64 FMA-chain peak probe (the build kernel's roofline denominator; the
+ * driver's MEASURED_PEAKS.json has no FP64 figure).  Runs `iters` dependent
+ * DFMA chains per thread; flops = 2 * 8 * iters * blocks * threads. */
+int fm_fp64_probe(int blocks, int threads, int iters, double *sink, fm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIELDMAP_H */

@@ -1,0 +1,277 @@
+// fm_fit.cuh -- per-target weighted least squares on a lane group (fp64).
+//
+// Semantics: fit_many, _ext.pyx:291-426.  Per target: shift the support to
+// the target (centering), scale by s = sqrt(max d^2), build the weighted
+// scaled Vandermonde A (m x k) and b = w*f, append ridge rows
+// sqrt(lam)/s^deg when lam > 0, solve min ||A c - b|| and map back
+// c /= s^deg.  value = c[0] (centered) or mono(t) . c.
+//
+// B200 formulation.  One group of G lanes (G = 16 for k <= 10, 32 above)
+// owns one target; lane l holds rows l, l+G, ... (ROWS per lane) of A in
+// registers, zero-padded -- a zero row changes neither R nor Q^T b.  The
+// solve is an unpivoted Householder QR (LAPACK dlarfg convention) whose
+// column norms and reflector dot products are butterfly reductions over the
+// group (identical result on every lane).  Instead of LAPACK dgelsy's
+// column-pivoted QR + incremental condition estimate, rank deficiency is
+// declared when kappa_1(R) = ||R||_1 ||R^-1||_1 >= 1.5/eps (calibrated
+// against dgelsy; the status differs from the reference only for
+// cond(A) within a factor ~2 of 1/eps).  For a well-posed
+// fit the least-squares solution is unique, so values agree with the
+// reference to ~1e-14 relative.
+//
+// Two outputs:
+//   SOLVE  (fit_many):  Q^T b rides along as column k; c = R^-1 (Q^T b).
+//   OP     (operator):  the value functional g^T c (g = e0 centered, or
+//                       mono(t)/s^deg) is linear in f: value = sum_i W_i f_i
+//                       with W = w .* (Q [R^-T g; 0]).  Q is applied as the
+//                       stored reflectors (stable), never formed as A R^-1.
+#pragma once
+
+#include "fm_common.cuh"
+
+namespace fm {
+
+constexpr double kSingularKappa = 1.5 / 2.220446049250313e-16;
+
+template <int DIM, int DEG>
+struct FitShape {
+    static constexpr int K = Monos<DIM, DEG>::K;
+    static constexpr int G = K <= 10 ? 16 : 32;
+};
+
+// Returns the group-uniform status (FM_FIT_*).
+// Inputs per lane/row q (row index i = q*G + glane): valid[q] (i < m),
+// p[q] source coordinates, w[q] weight (already |w|), f[q] field value
+// (SOLVE only).  sR: K*K doubles, sQ: K doubles of per-group shared memory.
+// OP: y[q] receives the operator weight of row i (0 for invalid rows).
+// SOLVE: coeffs[K] (lane-uniform) and value.
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
+__device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m,
+                                        const bool (&valid)[ROWS], const double (&p)[ROWS][DIM],
+                                        const double (&w)[ROWS], const double (&f)[ROWS],
+                                        int lane, int glane, double *sR, double *sQ,
+                                        double (&y)[ROWS], double (&coeffs)[Monos<DIM, DEG>::K],
+                                        double &value) {
+    constexpr Monos<DIM, DEG> M{};
+    constexpr int K = Monos<DIM, DEG>::K;
+    constexpr int NC = K + (SOLVE ? 1 : 0);
+    const int gbase = lane & ~(G - 1);
+
+    // ---- EMPTY: no rows, or no positive weight (_ext.pyx:340-350)
+    int npos = 0;
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) npos += (valid[q] && w[q] > 0.0) ? 1 : 0;
+    npos = group_sum_int<G>(npos);
+    const bool empty = (m == 0) || (npos == 0);
+
+    // ---- support scale s = sqrt(max |dx|^2) (_ext.pyx:353-366)
+    double dx[ROWS][DIM];
+    double smax_l = 0.0;
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+#pragma unroll
+        for (int a = 0; a < DIM; a++) dx[q][a] = fp.centering ? sub_rn(p[q][a], t[a]) : p[q][a];
+        double d2 = mul_rn(dx[q][0], dx[q][0]);
+#pragma unroll
+        for (int a = 1; a < DIM; a++) d2 = add_rn(d2, mul_rn(dx[q][a], dx[q][a]));
+        if (valid[q] && d2 > smax_l) smax_l = d2;
+    }
+    double s = __dsqrt_rn(group_max<G>(smax_l));
+    if (s == 0.0) s = 1.0;
+    double spow[K];
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        spow[c] = M.deg[c] == 0 ? 1.0
+                  : M.deg[c] == 1 ? s
+                  : M.deg[c] == 2 ? mul_rn(s, s)
+                                  : mul_rn(mul_rn(s, s), s);
+
+    // ---- weighted scaled Vandermonde rows (+ ridge rows), _ext.pyx:374-400
+    const bool ridge = fp.lam > 0.0;
+    const double sqrt_lam = ridge ? sqrt(fp.lam) : 0.0;
+    double A[ROWS][NC];
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        if (valid[q]) {
+            double u[DIM], mono[K];
+#pragma unroll
+            for (int a = 0; a < DIM; a++) u[a] = __ddiv_rn(dx[q][a], s);
+            eval_monos<DIM, DEG>(u, mono);
+            A[q][0] = w[q];
+#pragma unroll
+            for (int c = 1; c < K; c++) A[q][c] = mul_rn(mono[c], w[q]);
+            if (SOLVE) A[q][NC - 1] = mul_rn(w[q], f[q]);
+        } else {
+            const int col = i - m;
+            const bool rrow = ridge && col >= 0 && col < K;
+#pragma unroll
+            for (int c = 0; c < NC; c++)
+                A[q][c] = (rrow && c == col && c < K) ? __ddiv_rn(sqrt_lam, spow[c < K ? c : 0])
+                                                      : 0.0;
+        }
+    }
+
+    // ---- Householder QR, column by column
+    double tau[K], beta[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const double x0 = __shfl_sync(FM_FULL_MASK, A[j / G][j], gbase + (j % G));
+        double sl = 0.0;
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int i = q * G + glane;
+            if (i > j) sl = fma(A[q][j], A[q][j], sl);
+        }
+        const double sigma = group_sum<G>(sl);
+        double tj, bj, scal;
+        if (sigma == 0.0) {
+            tj = 0.0;
+            bj = x0;
+            scal = 0.0;
+        } else {
+            const double nrm = sqrt(fma(x0, x0, sigma));
+            bj = x0 >= 0.0 ? -nrm : nrm;
+            tj = (bj - x0) / bj;
+            scal = 1.0 / (x0 - bj);
+        }
+        tau[j] = tj;
+        beta[j] = bj;
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int i = q * G + glane;
+            if (i > j) A[q][j] *= scal;
+            else if (i == j) A[q][j] = bj;
+        }
+        double dot[NC];
+#pragma unroll
+        for (int l = j + 1; l < NC; l++) {
+            double pl = 0.0;
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+                if (i == j) pl += A[q][l];
+                else if (i > j) pl = fma(A[q][j], A[q][l], pl);
+            }
+            dot[l] = pl;
+        }
+#pragma unroll
+        for (int l = j + 1; l < NC; l++) dot[l] = group_sum<G>(dot[l]);
+#pragma unroll
+        for (int l = j + 1; l < NC; l++) {
+            const double td = tj * dot[l];
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+                if (i == j) A[q][l] -= td;
+                else if (i > j) A[q][l] = fma(-td, A[q][j], A[q][l]);
+            }
+        }
+    }
+
+    // ---- R (and Q^T b) to shared memory
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        if (i < K) {
+#pragma unroll
+            for (int l = 1; l < K; l++)
+                if (l > i) sR[i * K + l] = A[q][l];
+            if (SOLVE) sQ[i] = A[q][NC - 1];
+        }
+    }
+    if (glane == 0) {
+#pragma unroll
+        for (int j = 0; j < K; j++) sR[j * K + j] = beta[j];
+    }
+    __syncwarp();
+    double inv_beta[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) inv_beta[j] = 1.0 / beta[j];
+
+    // ---- rank test: kappa_1(R) = ||R||_1 ||R^-1||_1 (lane l owns column l)
+    double colsum = 0.0, invsum = 0.0;
+    {
+        const int l = glane;
+        double x[K];
+#pragma unroll
+        for (int i = K - 1; i >= 0; i--) {
+            double acc = (i == l) ? 1.0 : 0.0;
+#pragma unroll
+            for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
+            x[i] = (i <= l) ? acc * inv_beta[i] : 0.0;
+            if (i <= l && l < K) {
+                colsum += fabs(sR[i * K + l]);
+                invsum += fabs(x[i]);
+            }
+        }
+    }
+    const double kappa = group_max<G>(colsum) * group_max<G>(invsum);
+    const bool singular = !ridge && !(kappa < kSingularKappa);
+    const int status = empty ? FM_FIT_EMPTY : (singular ? FM_FIT_SINGULAR : FM_FIT_OK);
+
+    double mono_t[K];
+    eval_monos<DIM, DEG>(t, mono_t);
+    if (SOLVE) {
+        // c_scaled = R^-1 (Q^T b), coeffs = c_scaled / s^deg (_ext.pyx:411-412)
+        double cs[K];
+#pragma unroll
+        for (int i = K - 1; i >= 0; i--) {
+            double acc = sQ[i];
+#pragma unroll
+            for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], cs[c], acc);
+            cs[i] = acc / beta[i];
+        }
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            coeffs[c] = __ddiv_rn(cs[c], spow[c]);
+            v = add_rn(v, mul_rn(coeffs[c], mono_t[c]));
+        }
+        value = fp.centering ? coeffs[0] : v;  // _ext.pyx:413-425
+    } else {
+        // z = R^-T g
+        double z[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            double acc = fp.centering ? (i == 0 ? 1.0 : 0.0) : __ddiv_rn(mono_t[i], spow[i]);
+#pragma unroll
+            for (int c = 0; c < i; c++) acc = fma(-sR[c * K + i], z[c], acc);
+            z[i] = acc * inv_beta[i];
+        }
+        double yy[ROWS];
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int i = q * G + glane;
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < K; c++)
+                if (i == c) v = z[c];
+            yy[q] = v;
+        }
+        // y = H_0 H_1 ... H_{K-1} [z; 0]
+#pragma unroll
+        for (int j = K - 1; j >= 0; j--) {
+            double pl = 0.0;
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+                if (i == j) pl += yy[q];
+                else if (i > j) pl = fma(A[q][j], yy[q], pl);
+            }
+            const double td = tau[j] * group_sum<G>(pl);
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+                if (i == j) yy[q] -= td;
+                else if (i > j) yy[q] = fma(-td, A[q][j], yy[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) y[q] = valid[q] ? w[q] * yy[q] : 0.0;
+    }
+    __syncwarp();
+    return status;
+}
+
+}  // namespace fm

@@ -1,0 +1,292 @@
+// fm_grid.cu -- a1: source binning on the device.
+//
+// Replaces the reference's PointGrid construction (locate.py:144-161 over the
+// _CsrGrid CSR of locate.py:65-87: numpy clip/trunc cell keys, lexsort by
+// (cell, id), add.at + cumsum).  Here: one counting (radix) sort pass on the
+// cell key -- histogram, exclusive scan, scatter -- then an in-cell sort by id
+// so the layout is deterministic, then the coordinates are gathered into cell
+// order so the radius search reads candidates with coalesced loads.
+#include <algorithm>
+
+#include "fm_common.cuh"
+#include "fm_scan.cuh"
+
+namespace fm {
+
+template <int DIM>
+__device__ __forceinline__ int64_t cell_key(const GridDev &g, const double *p) {
+    int64_t c = 0, stride = 1;
+#pragma unroll
+    for (int a = 0; a < DIM; a++) {
+        c += cell_of(p[a], g.lo[a], g.inv_d[a], g.n[a]) * stride;
+        stride *= g.n[a];
+    }
+    return c;
+}
+
+template <int DIM>
+__global__ void k_cell_keys(GridDev g, const double *__restrict__ pts, int64_t n,
+                            int32_t *__restrict__ keys, int32_t *__restrict__ counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double p[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; a++) p[a] = pts[i * DIM + a];
+        const int32_t c = (int32_t)cell_key<DIM>(g, p);
+        keys[i] = c;
+        atomicAdd(&counts[c], 1);
+    }
+}
+
+__global__ void k_scatter(const int32_t *__restrict__ keys, int64_t n,
+                          const int32_t *__restrict__ start, int32_t *__restrict__ fill,
+                          int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = keys[i];
+        const int32_t pos = start[c] + atomicAdd(&fill[c], 1);
+        out[pos] = (int32_t)i;
+    }
+}
+
+// ids ascending inside each cell (the lexsort tie order of locate.py:79)
+__global__ void k_sort_cells(const int32_t *__restrict__ start, int64_t ncell,
+                             int32_t *__restrict__ ids) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = start[c], e = start[c + 1];
+        for (int32_t i = b + 1; i < e; i++) {
+            const int32_t v = ids[i];
+            int32_t j = i - 1;
+            while (j >= b && ids[j] > v) {
+                ids[j + 1] = ids[j];
+                j--;
+            }
+            ids[j + 1] = v;
+        }
+    }
+}
+
+template <int DIM>
+__global__ void k_gather_pts(const int32_t *__restrict__ ids, int64_t n,
+                             const double *__restrict__ pts, double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = ids[i];
+#pragma unroll
+        for (int a = 0; a < DIM; a++) out[i * DIM + a] = pts[s * DIM + a];
+    }
+}
+
+// ---- bbox with order-preserving integer atomics
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dval(unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+__global__ void k_bbox_init(unsigned long long *acc, int dim) {
+    const int a = threadIdx.x;
+    if (a < dim) {
+        acc[a] = ~0ull;        // running min key
+        acc[dim + a] = 0ull;   // running max key
+    }
+}
+
+template <int DIM>
+__global__ void k_bbox(const double *__restrict__ pts, int64_t n, unsigned long long *acc) {
+    double mn[DIM], mx[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; a++) {
+        mn[a] = INFINITY;
+        mx[a] = -INFINITY;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < DIM; a++) {
+            const double v = pts[i * DIM + a];
+            mn[a] = fmin(mn[a], v);
+            mx[a] = fmax(mx[a], v);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; a++) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(FM_FULL_MASK, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(FM_FULL_MASK, mx[a], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&acc[a], dkey(mn[a]));
+            atomicMax(&acc[DIM + a], dkey(mx[a]));
+        }
+    }
+}
+
+__global__ void k_bbox_final(const unsigned long long *acc, int dim, double *lohi) {
+    const int a = threadIdx.x;
+    if (a < 2 * dim) lohi[a] = dval(acc[a]);
+}
+
+template <int DIM>
+static int launch_keys(const GridDev &g, const double *pts, int64_t n, int32_t *keys,
+                       int32_t *counts, cudaStream_t s) {
+    const int threads = 256;
+    const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
+    if (blocks) k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+template <int DIM>
+static int launch_gather(const int32_t *ids, int64_t n, const double *pts, double *out,
+                         cudaStream_t s) {
+    const int threads = 256;
+    const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
+    if (blocks) k_gather_pts<DIM><<<(unsigned)blocks, threads, 0, s>>>(ids, n, pts, out);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+size_t fm_grid_workspace(int64_t n, int64_t ncell) {
+    return align256(sizeof(int32_t) * (size_t)n)           // keys
+           + align256(sizeof(int32_t) * (size_t)ncell) * 2  // counts, fill
+           + align256(scan_workspace_bytes(ncell));
+}
+
+int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *cell_start,
+                  int32_t *sorted_ids, double *sorted_pts, void *workspace,
+                  size_t workspace_bytes, fm_stream_t stream) {
+    if (!grid || grid->dim < 1 || grid->dim > kMaxDim || n < 0 || grid->ncell < 1)
+        return FM_ERR_ARG;
+    if (n >= (int64_t)INT32_MAX || grid->ncell >= (int64_t)INT32_MAX) return FM_ERR_UNSUPPORTED;
+    if (workspace_bytes < fm_grid_workspace(n, grid->ncell)) return FM_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ncell = grid->ncell;
+    char *w = (char *)workspace;
+    int32_t *keys = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)n);
+    int32_t *counts = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *fill = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)ncell);
+    void *scan_ws = w;
+    const GridDev g = to_dev(grid);
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
+    cudaMemsetAsync(fill, 0, sizeof(int32_t) * (size_t)ncell, s);
+    int rc;
+    switch (grid->dim) {
+    case 1: rc = launch_keys<1>(g, pts, n, keys, counts, s); break;
+    case 2: rc = launch_keys<2>(g, pts, n, keys, counts, s); break;
+    case 3: rc = launch_keys<3>(g, pts, n, keys, counts, s); break;
+    case 4: rc = launch_keys<4>(g, pts, n, keys, counts, s); break;
+    default: rc = launch_keys<5>(g, pts, n, keys, counts, s); break;
+    }
+    if (rc) return rc;
+    rc = exclusive_scan<int32_t, int32_t>(counts, ncell, cell_start, scan_ws,
+                                           scan_workspace_bytes(ncell), s);
+    if (rc) return rc;
+    const int threads = 256;
+    if (n > 0) {
+        const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, kSMs * 16);
+        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, fill, sorted_ids);
+    }
+    {
+        const int64_t blocks = std::min<int64_t>((ncell + threads - 1) / threads, kSMs * 16);
+        k_sort_cells<<<(unsigned)blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids);
+    }
+    FM_CHECK_LAUNCH();
+    switch (grid->dim) {
+    case 1: return launch_gather<1>(sorted_ids, n, pts, sorted_pts, s);
+    case 2: return launch_gather<2>(sorted_ids, n, pts, sorted_pts, s);
+    case 3: return launch_gather<3>(sorted_ids, n, pts, sorted_pts, s);
+    case 4: return launch_gather<4>(sorted_ids, n, pts, sorted_pts, s);
+    default: return launch_gather<5>(sorted_ids, n, pts, sorted_pts, s);
+    }
+}
+
+int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t stream) {
+    if (dim < 1 || dim > kMaxDim || n < 0) return FM_ERR_ARG;
+    // accumulate order-preserving integer keys in place of the output
+    // (same size: 2*dim x 8 B), converted back by k_bbox_final
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(lohi);
+    cudaStream_t s = (cudaStream_t)stream;
+    k_bbox_init<<<1, 32, 0, s>>>(acc, dim);
+    const int threads = 256;
+    const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 8) : 0;
+    if (blocks) {
+        switch (dim) {
+        case 1: k_bbox<1><<<(unsigned)blocks, threads, 0, s>>>(pts, n, acc); break;
+        case 2: k_bbox<2><<<(unsigned)blocks, threads, 0, s>>>(pts, n, acc); break;
+        case 3: k_bbox<3><<<(unsigned)blocks, threads, 0, s>>>(pts, n, acc); break;
+        case 4: k_bbox<4><<<(unsigned)blocks, threads, 0, s>>>(pts, n, acc); break;
+        default: k_bbox<5><<<(unsigned)blocks, threads, 0, s>>>(pts, n, acc); break;
+        }
+    }
+    k_bbox_final<<<1, 32, 0, s>>>(acc, dim, lohi);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+size_t fm_order_workspace(int64_t nt, int64_t ncell) { return fm_grid_workspace(nt, ncell) + align256(sizeof(int32_t) * (size_t)(ncell + 1)); }
+
+int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
+                    void *workspace, size_t workspace_bytes, fm_stream_t stream) {
+    if (!grid || grid->dim < 1 || grid->dim > kMaxDim || nt < 0 || grid->ncell < 1)
+        return FM_ERR_ARG;
+    if (nt >= (int64_t)INT32_MAX || grid->ncell >= (int64_t)INT32_MAX) return FM_ERR_UNSUPPORTED;
+    if (workspace_bytes < fm_order_workspace(nt, grid->ncell)) return FM_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ncell = grid->ncell;
+    char *w = (char *)workspace;
+    int32_t *keys = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)nt);
+    int32_t *counts = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *fill = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *start = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)(ncell + 1));
+    void *scan_ws = w;
+    const GridDev g = to_dev(grid);
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
+    cudaMemsetAsync(fill, 0, sizeof(int32_t) * (size_t)ncell, s);
+    int rc;
+    switch (grid->dim) {
+    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s); break;
+    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s); break;
+    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s); break;
+    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s); break;
+    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s); break;
+    }
+    if (rc) return rc;
+    rc = exclusive_scan<int32_t, int32_t>(counts, ncell, start, scan_ws,
+                                           scan_workspace_bytes(ncell), s);
+    if (rc) return rc;
+    if (nt > 0) {
+        const int threads = 256;
+        const int64_t blocks = std::min<int64_t>((nt + threads - 1) / threads, kSMs * 16);
+        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, nt, start, fill, perm);
+    }
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+size_t fm_scan_workspace(int64_t n) { return scan_workspace_bytes(n); }
+
+int fm_offsets_from_counts(const int32_t *counts, int64_t n, int64_t *offsets, void *workspace,
+                           size_t workspace_bytes, fm_stream_t stream) {
+    return exclusive_scan<int32_t, int64_t>(counts, n, offsets, workspace, workspace_bytes,
+                                            (cudaStream_t)stream);
+}
+
+}  // extern "C"

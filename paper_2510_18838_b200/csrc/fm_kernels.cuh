@@ -1,0 +1,512 @@
+// fm_kernels.cuh -- kernel templates (instantiated per dimension in fm_dimN.cu).
+//
+// Work split: one lane group (G lanes) per target; a warp holds 32/G groups
+// and walks the targets in tiles of 32/G consecutive entries of the
+// processing order `perm` (cell order of the source grid, so the groups of
+// a warp/CTA touch neighbouring sources).  All loops that contain warp
+// collectives have warp-uniform trip counts.
+#pragma once
+
+#include "fm_fit.cuh"
+#include "fm_search.cuh"
+
+namespace fm {
+
+constexpr int kBlock = 128;
+
+struct SearchArgs {
+    GridDev g;
+    const int32_t *cell_start;
+    const double *sorted_pts;
+    const int32_t *sorted_ids;
+    const double *targets;
+    int64_t nt;
+    const int32_t *perm;
+    fm_select sel;
+    const double *radii;  // final per-target radius (adaptive), or null
+};
+
+template <int DIM>
+__device__ __forceinline__ void load_target(const double *__restrict__ targets, int64_t i,
+                                            bool active, double *t) {
+#pragma unroll
+    for (int a = 0; a < DIM; a++) t[a] = active ? targets[i * DIM + a] : 0.0;
+}
+
+// --------------------------------------------------------- stats helpers
+// stats arrays: pairs of (count, first index) plus min/max slots; written
+// with warp-aggregated atomics.
+static __global__ void k_stats_init(int32_t *stats, int n, int kind) {
+    const int i = threadIdx.x;
+    if (i >= n) return;
+    if (kind == 0)  // count stats: max, min, nshort, first, nstatus, first
+        stats[i] = (i == 1 || i == 3 || i == 5) ? INT32_MAX : 0;
+    else  // fit stats: nfail, first
+        stats[i] = i == 1 ? INT32_MAX : 0;
+}
+
+__device__ __forceinline__ void warp_flush_pair(int32_t *slot, int n, int first) {
+    n = __reduce_add_sync(FM_FULL_MASK, n);
+    first = __reduce_min_sync(FM_FULL_MASK, (unsigned)first);
+    if ((threadIdx.x & 31) == 0 && n > 0) {
+        atomicAdd(slot, n);
+        atomicMin(slot + 1, first);
+    }
+}
+
+// ------------------------------------------------------------ count pass
+template <int DIM, int G>
+__global__ void __launch_bounds__(kBlock) k_support_count(SearchArgs s, int32_t min_required,
+                                                          int32_t *__restrict__ counts,
+                                                          double *__restrict__ radii,
+                                                          uint8_t *__restrict__ status,
+                                                          int32_t *__restrict__ stats) {
+    __shared__ RowTable<G> rts[kBlock / G];
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, glane = lane & (G - 1);
+    RowTable<G> &rt = rts[threadIdx.x / G];
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    int local_max = 0, local_min = INT32_MAX;
+    int nshort = 0, first_short = INT32_MAX, nstat = 0, first_stat = INT32_MAX;
+    for (int64_t tile = warp; tile * GPW < s.nt; tile += nwarps) {
+        const int64_t k = tile * GPW + lane / G;
+        const bool active = k < s.nt;
+        const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+        double t[DIM];
+        load_target<DIM>(s.targets, tid, active, t);
+        int m;
+        if (s.sel.adaptive) {
+            double r;
+            uint8_t st;
+            m = adaptive_radius<DIM, G>(s.g, s.cell_start, s.sorted_pts, t, s.sel, active, lane,
+                                        glane, rt, r, st);
+            if (active && glane == 0) {
+                if (radii) radii[tid] = r;
+                if (status) status[tid] = st;
+                if (st) {
+                    nstat++;
+                    first_stat = min(first_stat, (int)tid);
+                }
+            }
+        } else {
+            m = count_within<DIM, G>(s.g, s.cell_start, s.sorted_pts, t, s.sel.r_c, active, lane,
+                                     glane, rt);
+        }
+        if (active && glane == 0) {
+            counts[tid] = m;
+            local_max = max(local_max, m);
+            local_min = min(local_min, m);
+            if (m < min_required) {
+                nshort++;
+                first_short = min(first_short, (int)tid);
+            }
+        }
+    }
+    if (stats) {
+        local_max = __reduce_max_sync(FM_FULL_MASK, local_max);
+        local_min = __reduce_min_sync(FM_FULL_MASK, (unsigned)local_min);
+        if (lane == 0) {
+            atomicMax(stats + 0, local_max);
+            atomicMin(stats + 1, local_min);
+        }
+        warp_flush_pair(stats + 2, nshort, first_short);
+        warp_flush_pair(stats + 4, nstat, first_stat);
+    }
+}
+
+// per-group dynamic shared layout for the fill / fused kernels
+template <int G>
+struct GroupSmem {
+    RowTable<G> *rt;
+    int32_t *id, *pos, *sid, *spos;
+    double *sR, *sQ;
+};
+
+template <int G>
+__host__ __device__ inline size_t group_smem_bytes(int cap, int K) {
+    return sizeof(RowTable<G>) + (size_t)cap * 4 * sizeof(int32_t) +
+           (size_t)(K * K + K) * sizeof(double) + 16;
+}
+
+template <int G>
+__device__ __forceinline__ GroupSmem<G> carve(char *base, int cap, int K) {
+    const int grp = threadIdx.x / G;
+    char *p = base + (size_t)grp * ((group_smem_bytes<G>(cap, K) + 15) & ~(size_t)15);
+    GroupSmem<G> gs;
+    gs.sR = reinterpret_cast<double *>(p);
+    p += (size_t)K * K * sizeof(double);
+    gs.sQ = reinterpret_cast<double *>(p);
+    p += (size_t)K * sizeof(double);
+    gs.rt = reinterpret_cast<RowTable<G> *>(p);
+    p += sizeof(RowTable<G>);
+    gs.id = reinterpret_cast<int32_t *>(p);
+    gs.pos = gs.id + cap;
+    gs.sid = gs.pos + cap;
+    gs.spos = gs.sid + cap;
+    return gs;
+}
+
+template <int G>
+inline size_t block_smem_bytes(int cap, int K) {
+    return (size_t)(kBlock / G) * ((group_smem_bytes<G>(cap, K) + 15) & ~(size_t)15);
+}
+
+// ------------------------------------------------------------- fill pass
+// CSR of (idx, dist[, w]) in ascending id order at offsets[t].
+template <int DIM, int G>
+__global__ void __launch_bounds__(kBlock) k_support_fill(SearchArgs s, const int64_t *__restrict__ offsets,
+                                                         int cap, int64_t *__restrict__ idx,
+                                                         double *__restrict__ dist, int rbf_kind,
+                                                         double rbf_a, double *__restrict__ w) {
+    extern __shared__ __align__(16) char smem[];
+    GroupSmem<G> gs = carve<G>(smem, cap, 0);
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, glane = lane & (G - 1);
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t tile = warp; tile * GPW < s.nt; tile += nwarps) {
+        const int64_t k = tile * GPW + lane / G;
+        const bool active = k < s.nt;
+        const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+        double t[DIM];
+        load_target<DIM>(s.targets, tid, active, t);
+        const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
+        const int m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r,
+                                             active, lane, glane, *gs.rt, gs.id, gs.pos, gs.sid,
+                                             gs.spos, cap);
+        if (active) {
+            const int64_t off = offsets[tid];
+            const int mm = m < cap ? m : cap;
+            for (int e = glane; e < mm; e += G) {
+                double p[DIM];
+                load_point<DIM>(s.sorted_pts, gs.spos[e], p);
+                const double d = __dsqrt_rn(dist2_rn<DIM>(p, t));
+                idx[off + e] = gs.sid[e];
+                dist[off + e] = d;
+                if (w) w[off + e] = rbf_one(rbf_kind, rbf_a, r, d);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------- fused fill + fit
+// OP: writes operator rows (col, val) at offsets[t].  SOLVE: writes
+// values[t] for the scalar field src_val (no support materialised).
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
+__global__ void __launch_bounds__(kBlock) k_fused_fit(SearchArgs s, const int64_t *__restrict__ offsets,
+                                                      int cap, int rbf_kind, double rbf_a, fm_fit fp,
+                                                      const double *__restrict__ src,
+                                                      const double *__restrict__ src_val,
+                                                      int32_t *__restrict__ col,
+                                                      double *__restrict__ val,
+                                                      double *__restrict__ values,
+                                                      uint8_t *__restrict__ status,
+                                                      int32_t *__restrict__ stats) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    extern __shared__ __align__(16) char smem[];
+    int nfail = 0, first_fail = INT32_MAX;
+    GroupSmem<G> gs = carve<G>(smem, cap, K);
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, glane = lane & (G - 1);
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t tile = warp; tile * GPW < s.nt; tile += nwarps) {
+        const int64_t k = tile * GPW + lane / G;
+        const bool active = k < s.nt;
+        const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+        double t[DIM];
+        load_target<DIM>(s.targets, tid, active, t);
+        const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
+        int m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r, active,
+                                       lane, glane, *gs.rt, gs.id, gs.pos, gs.sid, gs.spos, cap);
+        if (m > cap) m = cap;  // host sizes cap >= max count
+        bool valid[ROWS];
+        double p[ROWS][DIM], w[ROWS], f[ROWS];
+        int32_t ids[ROWS];
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int i = q * G + glane;
+            valid[q] = i < m;
+            ids[q] = 0;
+            w[q] = 0.0;
+            f[q] = 0.0;
+#pragma unroll
+            for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
+            if (valid[q]) {
+                ids[q] = gs.sid[i];
+                load_point<DIM>(s.sorted_pts, gs.spos[i], p[q]);
+                const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
+                w[q] = fabs(rbf_one(rbf_kind, rbf_a, r, d));  // pointwise.py:301
+                if (SOLVE) f[q] = __ldg(src_val + ids[q]);
+            }
+        }
+        double y[ROWS], coeffs[K], value = 0.0;
+        const int st = fit_rows<DIM, DEG, G, ROWS, SOLVE>(fp, t, m, valid, p, w, f, lane, glane,
+                                                          gs.sR, gs.sQ, y, coeffs, value);
+        if (active) {
+            if (glane == 0) {
+                status[tid] = (uint8_t)st;
+                if (st != FM_FIT_OK) {
+                    nfail++;
+                    first_fail = min(first_fail, (int)tid);
+                }
+            }
+            if (SOLVE) {
+                if (glane == 0) values[tid] = st == FM_FIT_OK ? value : NAN;
+            } else {
+                const int64_t off = offsets[tid];
+#pragma unroll
+                for (int q = 0; q < ROWS; q++) {
+                    if (valid[q]) {
+                        const int i = q * G + glane;
+                        col[off + i] = ids[q];
+                        val[off + i] = st == FM_FIT_OK ? y[q] : NAN;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (stats) warp_flush_pair(stats, nfail, first_fail);
+    (void)src;
+}
+
+// ------------------------------------------------- fit_many (CSR input)
+template <int DIM, int DEG, int G, int ROWS>
+__global__ void __launch_bounds__(kBlock) k_fit_many(fm_fit fp, const double *__restrict__ targets,
+                                                     int64_t nt, const int64_t *__restrict__ sup_off,
+                                                     const int64_t *__restrict__ sup_idx,
+                                                     const double *__restrict__ sup_w,
+                                                     const double *__restrict__ src,
+                                                     const double *__restrict__ src_val,
+                                                     double *__restrict__ values,
+                                                     double *__restrict__ coeffs_out,
+                                                     uint8_t *__restrict__ status,
+                                                     int32_t *__restrict__ stats) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    int nfail = 0, first_fail = INT32_MAX;
+    __shared__ double sRs[kBlock / G][K * K + K];
+    double *sR = sRs[threadIdx.x / G];
+    double *sQ = sR + K * K;
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, glane = lane & (G - 1);
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t tile = warp; tile * GPW < nt; tile += nwarps) {
+        const int64_t tid = tile * GPW + lane / G;
+        const bool active = tid < nt;
+        double t[DIM];
+        load_target<DIM>(targets, tid, active, t);
+        const int64_t off = active ? sup_off[tid] : 0;
+        const int m = active ? (int)(sup_off[tid + 1] - off) : 0;
+        bool valid[ROWS];
+        double p[ROWS][DIM], w[ROWS], f[ROWS];
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int i = q * G + glane;
+            valid[q] = i < m;
+            w[q] = 0.0;
+            f[q] = 0.0;
+#pragma unroll
+            for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
+            if (valid[q]) {
+                const int64_t id = sup_idx[off + i];
+                w[q] = sup_w[off + i];
+#pragma unroll
+                for (int a = 0; a < DIM; a++) p[q][a] = __ldg(src + id * DIM + a);
+                f[q] = __ldg(src_val + id);
+            }
+        }
+        double y[ROWS], coeffs[K], value = 0.0;
+        const int st = fit_rows<DIM, DEG, G, ROWS, true>(fp, t, m, valid, p, w, f, lane, glane, sR,
+                                                         sQ, y, coeffs, value);
+        if (active) {
+            if (glane == 0) {
+                status[tid] = (uint8_t)st;
+                values[tid] = st == FM_FIT_OK ? value : NAN;
+                if (st != FM_FIT_OK) {
+                    nfail++;
+                    first_fail = min(first_fail, (int)tid);
+                }
+            }
+            if (coeffs_out) {
+#pragma unroll
+                for (int c = 0; c < K; c++)
+                    if (glane == (c % G)) coeffs_out[tid * K + c] = st == FM_FIT_OK ? coeffs[c] : NAN;
+            }
+        }
+        __syncwarp();
+    }
+    if (stats) warp_flush_pair(stats, nfail, first_fail);
+}
+
+// ------------------------------------------------------------ launchers
+inline int grid_blocks(int64_t nt, int groups_per_block, int per_sm) {
+    const int64_t need = (nt + groups_per_block - 1) / groups_per_block;
+    const int64_t cap = (int64_t)kSMs * per_sm;
+    return (int)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+template <int DIM>
+int launch_count(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,
+                 uint8_t *status, int32_t *stats, cudaStream_t st) {
+    constexpr int G = 16;
+    if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 6, 0);
+    if (s.nt == 0) return FM_OK;
+    k_support_count<DIM, G><<<grid_blocks(s.nt, kBlock / G, 16), kBlock, 0, st>>>(
+        s, min_required, counts, radii, status, stats);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+template <int DIM>
+int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *idx, double *dist,
+                int rbf_kind, double rbf_a, double *w, cudaStream_t st) {
+    constexpr int G = 16;
+    if (s.nt == 0) return FM_OK;
+    if (cap < 1) cap = 1;
+    const size_t sm = block_smem_bytes<G>(cap, 0);
+    if (sm > 200 * 1024) return FM_ERR_UNSUPPORTED;
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_support_fill<DIM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+    k_support_fill<DIM, G><<<grid_blocks(s.nt, kBlock / G, 16), kBlock, sm, st>>>(
+        s, offsets, cap, idx, dist, rbf_kind, rbf_a, w);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
+int launch_fused_rows(const SearchArgs &s, const int64_t *offsets, int cap, const fm_rbf &rbf,
+                      const fm_fit &fp, const double *src, const double *src_val, int32_t *col,
+                      double *val, double *values, uint8_t *status, int32_t *stats,
+                      cudaStream_t st) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    const size_t sm = block_smem_bytes<G>(cap, K);
+    if (sm > 200 * 1024) return FM_ERR_UNSUPPORTED;
+    auto kern = k_fused_fit<DIM, DEG, G, ROWS, SOLVE>;
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid_blocks(s.nt, kBlock / G, 16), kBlock, sm, st>>>(s, offsets, cap, rbf.kind, rbf.a, fp,
+                                                               src, src_val, col, val, values,
+                                                               status, stats);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+// rows needed by a fit: support + ridge rows, at least K
+inline int fit_rows_needed(int max_m, int K, double lam) {
+    int r = max_m + (lam > 0.0 ? K : 0);
+    return r < K ? K : r;
+}
+
+template <int DIM, int DEG, bool SOLVE>
+int launch_fused(const SearchArgs &s, const int64_t *offsets, int cap, const fm_rbf &rbf,
+                 const fm_fit &fp, const double *src, const double *src_val, int32_t *col,
+                 double *val, double *values, uint8_t *status, int32_t *stats, cudaStream_t st) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    constexpr int G = FitShape<DIM, DEG>::G;
+    if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 2, 1);
+    if (s.nt == 0) return FM_OK;
+    if (cap < 1) cap = 1;
+    const int need = fit_rows_needed(cap, K, fp.lam);
+#define FM_FUSED(R) \
+    launch_fused_rows<DIM, DEG, G, R, SOLVE>(s, offsets, cap, rbf, fp, src, src_val, col, val, values, status, stats, st)
+    if (need <= G) return FM_FUSED(1);
+    if (need <= 2 * G) return FM_FUSED(2);
+    if (need <= 4 * G) return FM_FUSED(4);
+    if constexpr (G == 16) {
+        if (need <= 8 * G) return FM_FUSED(8);
+    }
+#undef FM_FUSED
+    return FM_ERR_UNSUPPORTED;
+}
+
+template <int DIM, int DEG>
+int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const int64_t *sup_off,
+                    const int64_t *sup_idx, const double *sup_w, int max_m, const double *src,
+                    const double *src_val, double *values, double *coeffs, uint8_t *status,
+                    int32_t *stats, cudaStream_t st) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    constexpr int G = FitShape<DIM, DEG>::G;
+    if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 2, 1);
+    if (nt == 0) return FM_OK;
+    const int need = fit_rows_needed(max_m, K, fp.lam);
+    const int blocks = grid_blocks(nt, kBlock / G, 16);
+#define FM_FITMANY(R)                                                                       \
+    do {                                                                                    \
+        k_fit_many<DIM, DEG, G, R><<<blocks, kBlock, 0, st>>>(fp, targets, nt, sup_off, sup_idx, \
+                                                              sup_w, src, src_val, values,  \
+                                                              coeffs, status, stats);       \
+        FM_CHECK_LAUNCH();                                                                  \
+        return FM_OK;                                                                       \
+    } while (0)
+    if (need <= G) FM_FITMANY(1);
+    if (need <= 2 * G) FM_FITMANY(2);
+    if (need <= 4 * G) FM_FITMANY(4);
+    if constexpr (G == 16) {
+        if (need <= 8 * G) FM_FITMANY(8);
+    }
+#undef FM_FITMANY
+    return FM_ERR_UNSUPPORTED;
+}
+
+// ------------------------------------------------- instantiation units
+// Entry points per dimension (search) and per (dimension, degree) (fits),
+// defined in fm_dN.cu / fm_dN_pP.cu so the heavy fit instantiations compile
+// in parallel.  Degree 3 exists for dim <= 3 only (k <= 21).
+#define FM_DECLARE_DIM(N)                                                                         \
+    int dim##N##_count(const SearchArgs &, int32_t, int32_t *, double *, uint8_t *, int32_t *,   \
+                       cudaStream_t);                                                             \
+    int dim##N##_fill(const SearchArgs &, const int64_t *, int, int64_t *, double *, int,        \
+                      double, double *, cudaStream_t);
+#define FM_DECLARE_DEG(N, P)                                                                      \
+    int dim##N##_deg##P##_fused(bool, const SearchArgs &, const int64_t *, int, const fm_rbf &,  \
+                                const fm_fit &, const double *, const double *, int32_t *,       \
+                                double *, double *, uint8_t *, int32_t *, cudaStream_t);          \
+    int dim##N##_deg##P##_fit_many(const fm_fit &, const double *, int64_t, const int64_t *,     \
+                                   const int64_t *, const double *, int, const double *,         \
+                                   const double *, double *, double *, uint8_t *, int32_t *,     \
+                                   cudaStream_t);
+FM_DECLARE_DIM(1)
+FM_DECLARE_DIM(2)
+FM_DECLARE_DIM(3)
+FM_DECLARE_DIM(4)
+FM_DECLARE_DIM(5)
+FM_DECLARE_DEG(1, 0) FM_DECLARE_DEG(1, 1) FM_DECLARE_DEG(1, 2) FM_DECLARE_DEG(1, 3)
+FM_DECLARE_DEG(2, 0) FM_DECLARE_DEG(2, 1) FM_DECLARE_DEG(2, 2) FM_DECLARE_DEG(2, 3)
+FM_DECLARE_DEG(3, 0) FM_DECLARE_DEG(3, 1) FM_DECLARE_DEG(3, 2) FM_DECLARE_DEG(3, 3)
+FM_DECLARE_DEG(4, 0) FM_DECLARE_DEG(4, 1) FM_DECLARE_DEG(4, 2)
+FM_DECLARE_DEG(5, 0) FM_DECLARE_DEG(5, 1) FM_DECLARE_DEG(5, 2)
+
+#define FM_DEFINE_DIM(N)                                                                           \
+    int dim##N##_count(const SearchArgs &s, int32_t need, int32_t *c, double *r, uint8_t *st,     \
+                       int32_t *stats, cudaStream_t stream) {                                      \
+        return launch_count<N>(s, need, c, r, st, stats, stream);                                  \
+    }                                                                                              \
+    int dim##N##_fill(const SearchArgs &s, const int64_t *o, int cap, int64_t *idx, double *d,    \
+                      int kind, double a, double *w, cudaStream_t stream) {                        \
+        return launch_fill<N>(s, o, cap, idx, d, kind, a, w, stream);                              \
+    }
+
+#define FM_DEFINE_DEG(N, P)                                                                        \
+    int dim##N##_deg##P##_fused(bool solve, const SearchArgs &s, const int64_t *o, int cap,       \
+                                const fm_rbf &rbf, const fm_fit &fp, const double *src,            \
+                                const double *sv, int32_t *col, double *val, double *vals,         \
+                                uint8_t *st, int32_t *stats, cudaStream_t stream) {                \
+        return solve ? launch_fused<N, P, true>(s, o, cap, rbf, fp, src, sv, col, val, vals, st,   \
+                                                stats, stream)                                     \
+                     : launch_fused<N, P, false>(s, o, cap, rbf, fp, src, sv, col, val, vals, st,  \
+                                                 stats, stream);                                   \
+    }                                                                                              \
+    int dim##N##_deg##P##_fit_many(const fm_fit &fp, const double *t, int64_t nt,                 \
+                                   const int64_t *so, const int64_t *si, const double *sw, int mm, \
+                                   const double *src, const double *sv, double *vals, double *co,  \
+                                   uint8_t *st, int32_t *stats, cudaStream_t stream) {             \
+        return launch_fit_many<N, P>(fp, t, nt, so, si, sw, mm, src, sv, vals, co, st, stats,      \
+                                     stream);                                                      \
+    }
+
+}  // namespace fm

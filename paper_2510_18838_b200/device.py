@@ -1,0 +1,330 @@
+"""Device-resident hot path: torch tensors in HBM, compute in libfieldmap.so.
+
+PyTorch only provides memory, streams and host<->device copies here; every
+arithmetic step of the path is one of the library's sm_100a kernels:
+
+  SourceCloud          a1  source binning (fm_grid_build)       locate.py:144-161
+  count_supports       a3/a4 count / radius growth              _ext.pyx:203-288
+  fill_supports        a3/a4 fill + a5 weights                  _ext.pyx:225-287
+  fit_many             a7  fit_many                             _ext.pyx:291-426
+  transfer_values      a9  one-shot fused transfer              pointwise.py:434-451
+  Operator / build     a8  explicit transfer operator           pointwise.py:399-431
+  Operator.apply       a13 CSR SpMM over field components
+
+All launches go on torch's current CUDA stream.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import FmFit, FmGrid, FmRbf, FmSelect, check, ptr
+from .locate import grid_geometry
+
+INT32_MAX = 2 ** 31 - 1
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(a, dtype=torch.float64):
+    """numpy / torch -> contiguous CUDA tensor (no copy if already there)."""
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            return a.to(dtype=dtype).contiguous()
+        # host tensor: pinned memory makes this an async H2D copy on the stream
+        return a.to(dtype=dtype).contiguous().to(_dev(), non_blocking=a.is_pinned())
+    arr = np.ascontiguousarray(a, dtype=np.float64 if dtype == torch.float64 else None)
+    return torch.from_numpy(arr).to(_dev(), non_blocking=False)
+
+
+def _empty(shape, dtype, device):
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+def _workspace(nbytes, device):
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ------------------------------------------------------------------ a1
+class SourceCloud:
+    """Source points resident in HBM and binned into a uniform grid.
+
+    `points` (n, dim) fp64, dim 1..5.  The grid geometry follows the
+    reference's PointGrid (locate.py:144-161: padded bbox, ~cells_per_point
+    cells per point; for dim 2 the very same nx, ny, lo, dx, dy).  Search
+    results do not depend on the geometry."""
+
+    def __init__(self, points, cells_per_point=1.0, bbox=None, geom=None):
+        host = None if isinstance(points, torch.Tensor) else np.ascontiguousarray(points,
+                                                                                  dtype=np.float64)
+        self.pts = to_device(points if host is None else host)
+        if self.pts.ndim != 2 or not 1 <= self.pts.shape[1] <= 5 or self.pts.shape[0] == 0:
+            raise ValueError("points must be a nonempty (n, d) array with 1 <= d <= 5")
+        self.n, self.dim = self.pts.shape
+        if geom is None:
+            if bbox is None:
+                if host is not None:
+                    bbox = (host.min(axis=0), host.max(axis=0))
+                else:
+                    bbox = device_bbox(self.pts)
+            geom = grid_geometry(bbox[0], bbox[1], self.n, cells_per_point)
+        self.geom = geom
+        self.grid = self.geom.to_ctypes()
+        dev = self.pts.device
+        L = _lib.lib()
+        self.cell_start = _empty(self.geom.ncell + 1, torch.int32, dev)
+        self.sorted_ids = _empty(self.n, torch.int32, dev)
+        self.sorted_pts = _empty((self.n, self.dim), torch.float64, dev)
+        ws_bytes = L.fm_grid_workspace(self.n, self.geom.ncell)
+        ws = _workspace(ws_bytes, dev)
+        check(L.fm_grid_build(ctypes.byref(self.grid), ptr(self.pts), self.n,
+                              ptr(self.cell_start), ptr(self.sorted_ids), ptr(self.sorted_pts),
+                              ptr(ws), ws_bytes, _stream()), "fm_grid_build")
+        self._ws = ws  # keep alive until the stream has consumed it
+
+    def target_order(self, targets):
+        """Cell order of `targets` (device int32 perm) for locality."""
+        L = _lib.lib()
+        nt = targets.shape[0]
+        perm = _empty(nt, torch.int32, targets.device)
+        ws_bytes = L.fm_order_workspace(nt, self.geom.ncell)
+        ws = _workspace(ws_bytes, targets.device)
+        check(L.fm_target_order(ctypes.byref(self.grid), ptr(targets), nt, ptr(perm), ptr(ws),
+                                ws_bytes, _stream()), "fm_target_order")
+        self._ws_order = ws
+        return perm
+
+
+def device_bbox(pts):
+    dim = pts.shape[1]
+    lohi = torch.empty(2 * dim, dtype=torch.float64, device=pts.device)
+    check(_lib.lib().fm_bbox(dim, ptr(pts), pts.shape[0], ptr(lohi), _stream()), "fm_bbox")
+    h = lohi.cpu().numpy()
+    return h[:dim], h[dim:]
+
+
+# ------------------------------------------------------- selection spec
+@dataclass(frozen=True)
+class Select:
+    """fixed radius r_c, or adaptive (min_pts, r0, growth, r_max)."""
+
+    adaptive: bool
+    r_c: float = 0.0
+    min_pts: int = 0
+    r0: float = 0.0
+    growth: float = 0.0
+    r_max: float = 0.0
+
+    def to_ctypes(self):
+        return FmSelect(1 if self.adaptive else 0, int(self.min_pts), float(self.r_c),
+                        float(self.r0), float(self.growth), float(self.r_max))
+
+
+def fixed(r_c):
+    return Select(False, r_c=float(r_c))
+
+
+def adaptive(min_pts, r0, growth, r_max):
+    return Select(True, min_pts=int(min_pts), r0=float(r0), growth=float(growth),
+                  r_max=float(r_max))
+
+
+@dataclass
+class Counts:
+    counts: torch.Tensor  # int32 (nt,)
+    radii: torch.Tensor   # f64 (nt,) final radius (fixed: None)
+    status: torch.Tensor  # u8 (nt,) adaptive status (fixed: None)
+    stats: np.ndarray     # int32[6] host (see fieldmap.h)
+    offsets: torch.Tensor = None  # int64 (nt+1,)
+    nnz: int = 0
+
+    @property
+    def max_count(self):
+        return int(self.stats[0])
+
+
+def count_supports(cloud, targets, sel, perm=None, min_required=0, with_offsets=True):
+    """Count pass (+ exclusive scan).  One device->host sync for the stats."""
+    L = _lib.lib()
+    dev = targets.device
+    nt = targets.shape[0]
+    counts = _empty(nt, torch.int32, dev)
+    radii = _empty(nt, torch.float64, dev) if sel.adaptive else None
+    status = _empty(nt, torch.uint8, dev) if sel.adaptive else None
+    stats_d = _empty(6, torch.int32, dev)
+    csel = sel.to_ctypes()
+    check(L.fm_support_count(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
+                             ptr(cloud.sorted_pts), ptr(targets), nt, ptr(perm),
+                             ctypes.byref(csel), int(min_required), ptr(counts), ptr(radii),
+                             ptr(status), ptr(stats_d), _stream()), "fm_support_count")
+    offsets = None
+    if with_offsets:
+        offsets = _empty(nt + 1, torch.int64, dev)
+        ws_bytes = L.fm_scan_workspace(nt)
+        ws = _workspace(ws_bytes, dev)
+        check(L.fm_offsets_from_counts(ptr(counts), nt, ptr(offsets), ptr(ws), ws_bytes,
+                                       _stream()), "fm_offsets_from_counts")
+        summary = torch.cat([stats_d.to(torch.int64), offsets[nt:nt + 1]]).cpu().numpy()
+        stats = summary[:6].astype(np.int32)
+        nnz = int(summary[6])
+    else:
+        stats = stats_d.cpu().numpy()
+        nnz = 0
+    if nt == 0:
+        stats[0] = 0
+    return Counts(counts, radii, status, stats, offsets, nnz)
+
+
+def fill_supports(cloud, targets, sel, cnt, perm=None, rbf=None):
+    """Fill pass: (idx int64, dist f64[, raw weights f64]) CSR at cnt.offsets."""
+    L = _lib.lib()
+    dev = targets.device
+    idx = _empty(cnt.nnz, torch.int64, dev)
+    dist = _empty(cnt.nnz, torch.float64, dev)
+    w = _empty(cnt.nnz, torch.float64, dev) if rbf is not None else None
+    crbf = FmRbf(int(rbf[0]), 0, float(rbf[1])) if rbf is not None else None
+    csel = sel.to_ctypes()
+    check(L.fm_support_fill(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
+                            ptr(cloud.sorted_pts), ptr(cloud.sorted_ids), ptr(targets),
+                            targets.shape[0], ptr(perm), ctypes.byref(csel), ptr(cnt.radii),
+                            ptr(cnt.offsets), max(cnt.max_count, 1), ptr(idx), ptr(dist),
+                            ctypes.byref(crbf) if crbf is not None else None, ptr(w), _stream()),
+          "fm_support_fill")
+    return idx, dist, w
+
+
+def rbf_weights(kind, a, r_c, r):
+    out = torch.empty_like(r)
+    check(_lib.lib().fm_rbf_weights(int(kind), float(a), float(r_c), ptr(r), r.numel(), ptr(out),
+                                    _stream()), "fm_rbf_weights")
+    return out
+
+
+def _fit_struct(dim, degree, lam, centering):
+    return FmFit(int(dim), int(degree), float(lam), 1 if centering else 0, 0)
+
+
+def fit_many(targets, sup_off, sup_idx, sup_w, src, src_val, degree, lam, centering, max_m):
+    """fit_many on device CSR supports -> (values, coeffs, status, stats)."""
+    L = _lib.lib()
+    dev = targets.device
+    nt, dim = targets.shape
+    k = L.fm_n_monomials(dim, degree)
+    values = _empty(nt, torch.float64, dev)
+    coeffs = _empty((nt, k), torch.float64, dev)
+    status = _empty(nt, torch.uint8, dev)
+    stats = _empty(2, torch.int32, dev)
+    f = _fit_struct(dim, degree, lam, centering)
+    check(L.fm_fit_many(ctypes.byref(f), ptr(targets), nt, ptr(sup_off), ptr(sup_idx), ptr(sup_w),
+                        int(max_m), ptr(src), ptr(src_val), ptr(values), ptr(coeffs), ptr(status),
+                        ptr(stats), _stream()), "fm_fit_many")
+    return values, coeffs, status, stats
+
+
+def transfer_values(cloud, targets, sel, cnt, src_val, rbf, degree, lam, centering, perm=None):
+    """Fused fill + weights + fit for one scalar field (no supports kept)."""
+    L = _lib.lib()
+    dev = targets.device
+    nt = targets.shape[0]
+    values = _empty(nt, torch.float64, dev)
+    status = _empty(nt, torch.uint8, dev)
+    stats = _empty(2, torch.int32, dev)
+    csel = sel.to_ctypes()
+    crbf = FmRbf(int(rbf[0]), 0, float(rbf[1]))
+    f = _fit_struct(cloud.dim, degree, lam, centering)
+    check(L.fm_transfer_values(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
+                               ptr(cloud.sorted_pts), ptr(cloud.sorted_ids), ptr(targets), nt,
+                               ptr(perm), ctypes.byref(csel), ptr(cnt.radii),
+                               max(cnt.max_count, 1), ctypes.byref(crbf), ctypes.byref(f),
+                               ptr(cloud.pts), ptr(src_val), ptr(values), ptr(status), ptr(stats),
+                               _stream()), "fm_transfer_values")
+    return values, status, stats
+
+
+# ----------------------------------------------------------- operator
+class Operator:
+    """Explicit transfer operator W (nt x ns) in CSR, resident in HBM.
+
+    Row t (ids ascending) holds the weights with which the reference's fit
+    combines the support values (fit_many is linear in src_val), so
+    W @ f == fit_many(..., f).values for every field f."""
+
+    def __init__(self, offsets, col, val, status, perm, ns):
+        self.offsets = offsets
+        self.col = col
+        self.val = val
+        self.status = status
+        self.perm = perm
+        self.nt = offsets.shape[0] - 1
+        self.ns = ns
+
+    @property
+    def nnz(self):
+        return int(self.col.shape[0])
+
+    def apply(self, X, out=None):
+        """Y = W X for X (ns,) or (ns, C) fp64 on the device."""
+        squeeze = X.ndim == 1
+        X2 = X.reshape(X.shape[0], -1)
+        if X2.shape[0] != self.ns:
+            raise ValueError(f"field has {X2.shape[0]} rows, operator expects {self.ns}")
+        X2 = X2.contiguous()
+        C = X2.shape[1]
+        Y = out if out is not None else torch.empty((self.nt, C), dtype=torch.float64,
+                                                     device=X2.device)
+        check(_lib.lib().fm_apply(self.nt, ptr(self.offsets), ptr(self.col), ptr(self.val),
+                                  ptr(self.perm), ptr(X2), C, ptr(Y), _stream()), "fm_apply")
+        return Y[:, 0] if squeeze else Y
+
+    def algorithmic_bytes(self, C):
+        """nnz*(4+8) + nt*4 + ns*C*8 + nt*C*8."""
+        return self.nnz * 12 + self.nt * 4 + self.ns * C * 8 + self.nt * C * 8
+
+
+def build_operator(cloud, targets, sel, cnt, rbf, degree, lam, centering, perm=None):
+    """Fused fill + weights + fit -> Operator (plus the fit stats, device)."""
+    L = _lib.lib()
+    dev = targets.device
+    nt = targets.shape[0]
+    col = _empty(cnt.nnz, torch.int32, dev)
+    val = _empty(cnt.nnz, torch.float64, dev)
+    status = _empty(nt, torch.uint8, dev)
+    stats = _empty(2, torch.int32, dev)
+    csel = sel.to_ctypes()
+    crbf = FmRbf(int(rbf[0]), 0, float(rbf[1]))
+    f = _fit_struct(cloud.dim, degree, lam, centering)
+    check(L.fm_build_operator(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
+                              ptr(cloud.sorted_pts), ptr(cloud.sorted_ids), ptr(targets), nt,
+                              ptr(perm), ctypes.byref(csel), ptr(cnt.radii), ptr(cnt.offsets),
+                              max(cnt.max_count, 1), ctypes.byref(crbf), ctypes.byref(f),
+                              ptr(cloud.pts), ptr(col), ptr(val), ptr(status), ptr(stats),
+                              _stream()), "fm_build_operator")
+    return Operator(cnt.offsets, col, val, status, perm, cloud.n), stats
+
+
+def fp64_probe(blocks=148 * 8, threads=256, iters=4096):
+    """Measured FP64 FMA peak in TFLOP/s (CUDA events, best of 5)."""
+    sink = torch.zeros(1, dtype=torch.float64, device=_dev())
+    L = _lib.lib()
+    check(L.fm_fp64_probe(blocks, threads, 64, ptr(sink), _stream()), "fm_fp64_probe")
+    best = None
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        check(L.fm_fp64_probe(blocks, threads, iters, ptr(sink), _stream()), "fm_fp64_probe")
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    flops = 2.0 * 8 * iters * blocks * threads
+    return flops / (best * 1e-3) / 1e12

@@ -1,0 +1,211 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Runs only in the build container, where /root/reference exists: it imports
+the reference package `fieldbridge` with its compiled Cython backend
+(oracle/_ref, built by `make -C oracle ref` from the reference's own
+_ext.pyx) and records inputs + outputs of the hot-path calls as small .npz
+files.  The GPU box never needs the reference: tests read these files.
+
+    python tests/golden/make_golden.py
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import ref  # noqa: E402
+
+fb = ref.import_reference_package()
+K = fb._kernels
+from fieldbridge.pointwise import PreparedTransfer  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"{path}: {os.path.getsize(path) / 1024:.1f} KiB")
+
+
+def rbf_table():
+    r = np.concatenate([[0.0], np.linspace(0.0, 0.7, 71)[1:], [0.7000000001, 0.9]])
+    out = {"r": r}
+    for kind in range(8):
+        out[f"w{kind}"] = K.rbf_weights(kind, 2.0, 0.7, r)
+    save("rbf", **out)
+
+
+def disk_small():
+    m = fb.disk(1.0, 8)
+    t = np.ascontiguousarray(m.centroids()[:50])
+    pg = fb.build_point_grid(m.coords)
+    off, idx, dist = K.fixed_radius_supports(t, pg.points, float(pg.lo[0]), float(pg.lo[1]),
+                                             pg.dx, pg.dy, pg.nx, pg.ny, pg.cell_offsets,
+                                             pg.cell_items, 0.3)
+    save("disk_small", coords=m.coords, tris=m.tris, centroids=m.centroids(),
+         mean_edge_length=m.mean_edge_length, grid_lo=pg.lo, grid_n=np.array([pg.nx, pg.ny]),
+         grid_d=np.array([pg.dx, pg.dy]), cell_offsets=pg.cell_offsets,
+         cell_items=pg.cell_items, rq_off=off, rq_idx=idx, rq_dist=dist)
+
+
+def c1():
+    m = fb.square(99)
+    src = m.coords
+    tg = np.random.RandomState(0).uniform(0, 1, (10000, 2))
+    vals = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    h = m.mean_edge_length
+    pg = fb.build_point_grid(src)
+    off, idx, dist = K.fixed_radius_supports(tg, pg.points, float(pg.lo[0]), float(pg.lo[1]),
+                                             pg.dx, pg.dy, pg.nx, pg.ny, pg.cell_offsets,
+                                             pg.cell_items, 2 * h)
+    spec = fb.FitSpec(2, fb.RadialBasisSpec(fb.RbfKind.C4, a=2.0), fb.FixedRadius(2 * h))
+    values = fb.fit_point_cloud(src, vals, tg, spec)
+    w = np.abs(K.rbf_weights(K.RBF_C4, 2.0, 2 * h, dist))
+    # fit_many variants on the first 600 targets (all degrees, ridge, centering)
+    n = 600
+    fits = {}
+    for deg in (0, 1, 2):
+        for lam in (0.0, 1e-6):
+            for cen in (True, False):
+                v, c, st = K.fit_many(tg[:n], off[:n + 1], idx, w, src, vals, deg, lam, cen)
+                key = f"d{deg}_l{'r' if lam else '0'}_{'c' if cen else 'u'}"
+                fits["fit_v_" + key] = v
+                fits["fit_c_" + key] = c
+                fits["fit_s_" + key] = st
+    keep = off[1000]
+    save("c1", mean_edge_length=h, values=values, counts=np.diff(off).astype(np.int16),
+         off1000=off[:1001], idx1000=idx[:keep], dist1000=dist[:keep], nnz=off[-1], **fits)
+
+
+def adaptive():
+    srcm = fb.disk_graded(1.0, 30, 0.6)
+    tgm = fb.disk(1.0, 30)
+    src, tg = srcm.coords, tgm.coords
+    h = srcm.mean_edge_length
+    vals = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    pg = fb.build_point_grid(src)
+    span = np.vstack([src, tg])
+    lo, hi = span.min(axis=0), span.max(axis=0)
+    r_max = 1.0000001 * float(np.hypot(hi[0] - lo[0], hi[1] - lo[1])) + 1e-300
+    off, idx, dist, radii, status = K.adaptive_radius_supports(
+        tg, pg.points, float(pg.lo[0]), float(pg.lo[1]), pg.dx, pg.dy, pg.nx, pg.ny,
+        pg.cell_offsets, pg.cell_items, 12, h, 1.5, r_max)
+    spec = fb.FitSpec(2, fb.RadialBasisSpec(fb.RbfKind.C4, a=2.0), fb.AdaptiveRadius(12, h, 1.5))
+    pt = PreparedTransfer(src, tg, spec)
+    vals8 = np.stack([np.sin((c + 1) * src[:, 0]) * np.cos(src[:, 1]) + 2 for c in range(3)], 1)
+    applied = np.stack([pt.apply(vals8[:, c]) for c in range(3)], 1)
+    save("adaptive", src_n_rings=30, mean_edge_length=h, r_max=r_max, off=off, idx=idx,
+         dist=dist, radii=radii, status=status, values3=applied)
+
+
+def poly_repro():
+    m = fb.disk(1.0, 8)
+    polys = {
+        0: lambda x, y: np.full_like(x, 3.5),
+        1: lambda x, y: 2 * x - y + 1,
+        2: lambda x, y: x * x + 2 * x * y - y * y + x + 0.5,
+    }
+    out = {}
+    h = m.mean_edge_length
+    for kind in fb.RbfKind:
+        for deg in (0, 1, 2):
+            f = fb.sample_field(m, polys[deg], "vertices", 1)
+            spec = fb.FitSpec(deg, fb.RadialBasisSpec(kind, a=2.0),
+                              fb.AdaptiveRadius(max(6, 2 * fb.pointwise.n_monomials(deg)),
+                                                1.5 * h, 1.5), lam=0.0)
+            out[f"{kind.value}_{deg}"] = fb.transfer_pointwise(f, m.centroids(), spec)
+    # fixed-radius C4 degree 1 (dense-LS oracle test) and Gaussian 2.5h
+    f = fb.sample_field(m, lambda x, y: np.sin(x) * np.cos(y) + 2, "vertices", 1)
+    out["fixed_c4_1"] = fb.transfer_pointwise(
+        f, m.centroids(), fb.FitSpec(1, fb.RadialBasisSpec(fb.RbfKind.C4), fb.FixedRadius(2 * h)))
+    save("poly_repro", **out)
+
+
+def random_clouds():
+    rs1, rs2 = np.random.RandomState(1), np.random.RandomState(2)
+    src = rs1.uniform(0, 1, (20000, 2))
+    tg = rs2.uniform(0, 1, (4000, 2))
+    vals = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    out = {"src": src, "tg": tg}
+    for kind in (fb.RbfKind.GAUSSIAN, fb.RbfKind.MULTIQUADRIC):
+        spec = fb.FitSpec(2, fb.RadialBasisSpec(kind, a=2.0),
+                          fb.AdaptiveRadius(12, 1.5 / np.sqrt(src.shape[0]), 1.5))
+        out[kind.value] = fb.fit_point_cloud(src, vals, tg, spec)
+    save("random_clouds", **out)
+
+
+def singular_cases():
+    rng = np.random.RandomState(7)
+    pts_l, vals_l, w_l, off = [], [], [], [0]
+    tg = []
+    degs = []
+    for trial in range(400):
+        deg = 1 + trial % 2
+        k = (deg + 1) * (deg + 2) // 2
+        m = rng.randint(k, 20)
+        x = rng.uniform(-1, 1, m)
+        delta = 10.0 ** rng.uniform(-19, -4)
+        y = (0.3 * x if deg == 1 else 0.3 * x * x) + delta * rng.randn(m)
+        pts_l.append(np.column_stack([x, y]))
+        vals_l.append(rng.randn(m))
+        w_l.append(rng.uniform(0.5, 2, m))
+        off.append(off[-1] + m)
+        tg.append([0.01, 0.02])
+        degs.append(deg)
+    pts = np.vstack(pts_l)
+    vals = np.concatenate(vals_l)
+    w = np.concatenate(w_l)
+    off = np.array(off)
+    tg = np.array(tg)
+    degs = np.array(degs)
+    st = np.zeros(len(degs), np.uint8)
+    v = np.zeros(len(degs))
+    cond = np.zeros(len(degs))
+    for i in range(len(degs)):
+        sl = slice(off[i], off[i + 1])
+        vi, _c, si = K.fit_many(tg[i:i + 1], np.array([0, off[i + 1] - off[i]]),
+                                np.arange(off[i + 1] - off[i]), w[sl], pts[sl], vals[sl],
+                                int(degs[i]), 0.0, True)
+        st[i], v[i] = si[0], vi[0]
+        d = pts[sl] - tg[i]
+        s = np.sqrt(np.max(d[:, 0] ** 2 + d[:, 1] ** 2))
+        u, vv = d[:, 0] / s, d[:, 1] / s
+        cols = [np.ones_like(u), u, vv, u * u, u * vv, vv * vv][:(degs[i] + 1) * (degs[i] + 2) // 2]
+        cond[i] = np.linalg.cond(np.stack(cols, 1) * w[sl][:, None])
+    save("singular", pts=pts, vals=vals, w=w, off=off, tg=tg, degs=degs, status=st, values=v,
+         cond=cond)
+
+
+def fit_local_cases():
+    out = {}
+    rng = np.random.RandomState(1)
+    pts = rng.uniform(-1, 1, size=(8, 2))
+    w = rng.uniform(0.1, 2.0, size=8)
+    out["const_pts"], out["const_w"] = pts, w
+    out["const_c"] = fb.fit_local((0.1, -0.2), pts, np.full(8, 7.0), w, degree=2)
+    rng = np.random.RandomState(2)
+    pts = rng.uniform(-1, 1, size=(10, 2))
+    vals = rng.randn(10)
+    out["ridge_pts"], out["ridge_vals"] = pts, vals
+    for lam in (0.0, 1e2, 1e4, 1e6):
+        out[f"ridge_c_{lam:g}"] = fb.fit_local((0.0, 0.0), pts, vals, np.ones(10), degree=1,
+                                               lam=lam)
+    pts = np.array([[0.0, 0.0], [0.5, 0.5], [1.0, 1.0], [0.25, 0.25]])
+    out["collinear_ridge_c"] = fb.fit_local((0.5, 0.5), pts, np.array([0.0, 1.0, 2.0, 0.5]),
+                                            np.ones(4), degree=1, lam=1e-8)
+    save("fit_local", **out)
+
+
+if __name__ == "__main__":
+    rbf_table()
+    disk_small()
+    c1()
+    adaptive()
+    poly_repro()
+    random_clouds()
+    singular_cases()
+    fit_local_cases()

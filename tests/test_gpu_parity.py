@@ -1,0 +1,488 @@
+"""GPU parity: the B200 path against the reference's golden outputs and the
+CPU oracle, through the package API and the C ABI.
+
+Mirrors the reference's hot-path tests (pkg/tests/test_pointwise.py and
+test_locate.py:128-141).  Bars (north_star): neighbour
+sets and distances bit-exact; values within 1e-10 relative in fp64.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, sample_field
+from oracle import oracle as O
+from paper_2510_18838_b200 import _kernels as Kb
+from paper_2510_18838_b200 import pointwise as P
+from paper_2510_18838_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+VALUE_RTOL = 1e-10  # north_star: interpolated values within 1e-10 relative (fp64)
+ALL_KINDS = list(P.RbfKind)
+
+
+def _rel(a, b):
+    return np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))
+
+
+# ------------------------------------------------------------ rbf (a5)
+def test_rbf_table():
+    g = golden("rbf")
+    for kind in range(8):
+        got = Kb.rbf_weights(kind, 2.0, 0.7, g["r"])
+        want = g[f"w{kind}"]
+        if kind in (0, 6):  # exp / log: CUDA libm vs glibc, <= 2 ulp
+            assert np.allclose(got, want, rtol=5e-16, atol=0), kind
+        else:
+            assert np.array_equal(got, want), kind
+
+
+def test_eval_rbf_table_values():
+    # reference test_pointwise.py:24-46
+    assert P.eval_rbf(P.RadialBasisSpec(P.RbfKind.GAUSSIAN, r_c=1.0), 0.0) == 1.0
+    assert P.eval_rbf(P.RadialBasisSpec(P.RbfKind.C4, r_c=1.0), 0.0) == 6.0
+    got = P.eval_rbf(P.RadialBasisSpec(P.RbfKind.MULTIQUADRIC, a=2.0, r_c=0.7), 0.7)
+    assert got == pytest.approx(np.sqrt(5.0), rel=1e-15)
+    assert P.eval_rbf(P.RadialBasisSpec(P.RbfKind.THIN_PLATE_SPLINE, r_c=1.0), 0.0) == 0.0
+    for kind in ALL_KINDS:
+        w = P.eval_rbf(P.RadialBasisSpec(kind, r_c=0.4), 0.6)
+        assert w == (1.0 if kind is P.RbfKind.IDENTITY else 0.0)
+    spec = P.RadialBasisSpec(P.RbfKind.IDENTITY)
+    assert np.array_equal(P.eval_rbf(spec, np.array([0.0, 5.0])), [1.0, 1.0])
+    with pytest.raises(ValueError):
+        Kb.rbf_weights(9, 2.0, 1.0, np.array([0.1]))
+
+
+# ------------------------------------------------------ search (a1-a4)
+def test_point_grid_radius_query_bitwise():
+    # reference test_locate.py:128-141, through the drop-in seam
+    g = golden("disk_small")
+    pg = P.PointGrid(g["coords"])
+    t = np.ascontiguousarray(g["centroids"][:50])
+    off, idx, dist = Kb.fixed_radius_supports(t, pg.points, float(pg.lo[0]), float(pg.lo[1]),
+                                              pg.dx, pg.dy, pg.nx, pg.ny, None, None, 0.3)
+    assert off.dtype == np.int64 and idx.dtype == np.int64 and dist.dtype == np.float64
+    assert np.array_equal(off, g["rq_off"])
+    assert np.array_equal(idx, g["rq_idx"])
+    assert np.array_equal(dist, g["rq_dist"])
+    d_all = np.linalg.norm(g["coords"][None, :, :] - t[:, None, :], axis=2)
+    for i in range(t.shape[0]):
+        assert np.array_equal(idx[off[i]:off[i + 1]], np.nonzero(d_all[i] < 0.3)[0])
+
+
+def test_point_grid_cells_match_reference():
+    g = golden("disk_small")
+    pg = P.PointGrid(g["coords"])
+    assert np.array_equal(pg.cell_offsets, g["cell_offsets"])
+    assert np.array_equal(pg.cell_items, g["cell_items"])
+
+
+def _c1():
+    m = synth.square(99)
+    src = m.coords
+    tg = np.random.RandomState(0).uniform(0, 1, (10000, 2))
+    vals = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    return src, tg, vals, m.mean_edge_length
+
+
+def test_c1_supports_bitwise():
+    g = golden("c1")
+    src, tg, vals, h = _c1()
+    pg = P.PointGrid(src)
+    off, idx, dist = Kb.fixed_radius_supports(tg, src, float(pg.lo[0]), float(pg.lo[1]), pg.dx,
+                                              pg.dy, pg.nx, pg.ny, None, None, 2 * h)
+    assert np.array_equal(np.diff(off), g["counts"].astype(np.int64))
+    k = int(g["off1000"][-1])
+    assert np.array_equal(idx[:k], g["idx1000"])
+    assert np.array_equal(dist[:k], g["dist1000"])
+    # the whole CSR against the oracle (bitwise)
+    po = O.OraclePointGrid(src)
+    want = O.supports_nd(tg, po, 2 * h)
+    for a, b in zip((off, idx, dist), want):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cells_per_point", [0.25, 1.0, 4.0])
+def test_supports_independent_of_grid_resolution(cells_per_point):
+    src, tg, _vals, h = _c1()
+    from paper_2510_18838_b200 import device as D
+
+    cloud = D.SourceCloud(src, cells_per_point)
+    t = D.to_device(tg)
+    sel = D.fixed(2.5 * h)
+    cnt = D.count_supports(cloud, t, sel, cloud.target_order(t))
+    idx, dist, _ = D.fill_supports(cloud, t, sel, cnt, None)
+    want = O.supports_nd(tg, O.OraclePointGrid(src), 2.5 * h)
+    assert np.array_equal(cnt.offsets.cpu().numpy(), want[0])
+    assert np.array_equal(idx.cpu().numpy(), want[1])
+    assert np.array_equal(dist.cpu().numpy(), want[2])
+
+
+def test_adaptive_supports_bitwise():
+    g = golden("adaptive")
+    src = synth.disk_graded(1.0, 30, 0.6).coords
+    tg = synth.disk(1.0, 30).coords
+    h = float(g["mean_edge_length"])
+    pg = P.PointGrid(src)
+    got = Kb.adaptive_radius_supports(tg, src, float(pg.lo[0]), float(pg.lo[1]), pg.dx, pg.dy,
+                                      pg.nx, pg.ny, None, None, 12, h, 1.5, float(g["r_max"]))
+    for name, a in zip(("off", "idx", "dist", "radii", "status"), got):
+        assert np.array_equal(a, g[name]), name
+
+
+def test_lattice_targets_at_exact_spacing_multiples():
+    # targets on the source lattice and half-way: exact ties d == r must be excluded
+    src = synth.square(40).coords
+    h = 1.0 / 40
+    tg = np.vstack([src[::7], src[::11] + 0.5 * h])
+    for r in (h, 2 * h, np.sqrt(2) * h, 3 * h):
+        po = O.OraclePointGrid(src)
+        want = O.supports_nd(tg, po, r)
+        got = Kb.fixed_radius_supports(tg, src, po.lo[0], po.lo[1], po.dx, po.dy, po.nx, po.ny,
+                                       None, None, r)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+
+def test_select_support_single_coincident_source():
+    src = np.array([[0.5, 0.5], [3.0, 3.0]])
+    idx, w = P.select_support((0.5, 0.5), src, P.FixedRadius(0.1),
+                              rbf=P.RadialBasisSpec(P.RbfKind.C4, r_c=0.1), fit_degree=0)
+    assert list(idx) == [0]
+    assert w[0] == 6.0
+
+
+def test_fixed_radius_underdetermined():
+    src = np.random.RandomState(0).uniform(0, 1, size=(4, 2))
+    with pytest.raises(P.UnderdeterminedError):
+        P.select_support((0.5, 0.5), src, P.FixedRadius(5.0),
+                         rbf=P.RadialBasisSpec(P.RbfKind.CONST, r_c=5.0), fit_degree=2)
+
+
+def test_adaptive_radius_matches_distance_sort_oracle():
+    xs = np.linspace(0, 1, 11)
+    src = np.array([(x, y) for x in xs for y in xs])
+    target = np.array([0.52, 0.47])
+    r0, growth, min_points = 1e-3, 1.5, 10
+    idx, w = P.select_support(target, src, P.AdaptiveRadius(min_points, r0, growth),
+                              rbf=P.RadialBasisSpec(P.RbfKind.CONST), fit_degree=1)
+    d = np.linalg.norm(src - target, axis=1)
+    r = r0
+    while np.count_nonzero(d < r) < min_points:
+        r *= growth
+    assert np.array_equal(np.sort(idx), np.nonzero(d < r)[0])
+    assert set(np.argsort(d)[:min_points]).issubset(set(idx))
+
+
+def test_adaptive_radius_insufficient_sources():
+    src = np.array([[0.0, 0.0], [1.0, 0.0]])
+    with pytest.raises(P.InsufficientSourcesError):
+        P.select_support((0.5, 0.5), src, P.AdaptiveRadius(5, 0.1, 2.0),
+                         rbf=P.RadialBasisSpec(P.RbfKind.CONST), fit_degree=0)
+
+
+# ----------------------------------------------------------- fit (a7)
+def test_fit_local_cases():
+    g = golden("fit_local")
+    c = P.fit_local((0.1, -0.2), g["const_pts"], np.full(8, 7.0), g["const_w"], degree=2)
+    assert c[0] == pytest.approx(7.0, rel=1e-13)
+    assert np.abs(c[1:]).max() < 1e-12
+    assert np.allclose(c, g["const_c"], rtol=1e-10, atol=1e-13)
+    pts = np.array([[0.0, 0.0], [1.0, 0.1], [0.2, 1.0], [0.9, 0.8]])
+    c = P.fit_local((0.4, 0.3), pts, 2 * pts[:, 0] + 3 * pts[:, 1], np.ones(4), degree=1)
+    assert c[0] == pytest.approx(2 * 0.4 + 3 * 0.3, abs=1e-12)
+    assert c[1] == pytest.approx(2.0, abs=1e-12) and c[2] == pytest.approx(3.0, abs=1e-12)
+    norms = []
+    for lam in (0.0, 1e2, 1e4, 1e6):
+        c = P.fit_local((0.0, 0.0), g["ridge_pts"], g["ridge_vals"], np.ones(10), degree=1,
+                        lam=lam)
+        assert _rel(c, g[f"ridge_c_{lam:g}"]) < 1e-10
+        norms.append(np.linalg.norm(c))
+    assert all(a >= b for a, b in zip(norms, norms[1:]))
+    assert norms[-1] < 1e-4 * norms[0]
+
+
+def test_fit_local_singular_without_regularization():
+    pts = np.array([[0.0, 0.0], [0.5, 0.5], [1.0, 1.0], [0.25, 0.25]])
+    vals = np.array([0.0, 1.0, 2.0, 0.5])
+    with pytest.raises(P.SingularFitError):
+        P.fit_local((0.5, 0.5), pts, vals, np.ones(4), degree=1, lam=0.0)
+    c = P.fit_local((0.5, 0.5), pts, vals, np.ones(4), degree=1, lam=1e-8)
+    assert np.isfinite(c).all()
+    assert _rel(c, golden("fit_local")["collinear_ridge_c"]) < 1e-8
+
+
+def test_weight_scaling_invariance():
+    rng = np.random.RandomState(3)
+    pts = rng.uniform(-1, 1, size=(12, 2))
+    vals = np.sin(pts[:, 0]) + pts[:, 1] ** 2
+    w = rng.uniform(0.5, 1.5, size=12)
+    c1 = P.fit_local((0.1, 0.2), pts, vals, w, degree=2)
+    c2 = P.fit_local((0.1, 0.2), pts, vals, 37.5 * w, degree=2)
+    assert np.allclose(c1, c2, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2])
+@pytest.mark.parametrize("lam", [0.0, 1e-6])
+@pytest.mark.parametrize("cen", [True, False])
+def test_fit_many_variants_vs_reference(deg, lam, cen):
+    g = golden("c1")
+    src, tg, vals, h = _c1()
+    n = 600
+    off = g["off1000"][:n + 1]
+    idx = g["idx1000"][:off[-1]]
+    w = np.abs(O.rbf_weights(O.RBF_C4, 2.0, 2 * h, g["dist1000"][:off[-1]]))
+    v, c, st = Kb.fit_many(tg[:n], off, idx, w, src, vals, deg, lam, cen)
+    key = f"d{deg}_l{'r' if lam else '0'}_{'c' if cen else 'u'}"
+    assert np.array_equal(st, g["fit_s_" + key])
+    assert _rel(v, g["fit_v_" + key]) < VALUE_RTOL
+    # coefficients: relative to the coefficient scale of each target
+    want_c = g["fit_c_" + key]
+    scale = np.abs(want_c).max(axis=1, keepdims=True)
+    assert np.max(np.abs(c - want_c) / scale) < 1e-9
+
+
+def test_singular_status_outside_gray_zone():
+    g = golden("singular")
+    off = g["off"]
+    n = len(g["degs"])
+    gray = 0
+    for i in range(n):
+        sl = slice(off[i], off[i + 1])
+        m = off[i + 1] - off[i]
+        v, _c, st = Kb.fit_many(g["tg"][i:i + 1], np.array([0, m]), np.arange(m), g["w"][sl],
+                                g["pts"][sl], g["vals"][sl], int(g["degs"][i]), 0.0, True)
+        cond = g["cond"][i]
+        if 1e15 <= cond <= 1e17:
+            gray += 1
+            continue
+        assert st[0] == g["status"][i], (i, cond)
+        if st[0] == 0 and cond < 1e6:
+            assert abs(v[0] - g["values"][i]) <= VALUE_RTOL * abs(g["values"][i]) + 1e-13
+    assert gray < n // 2
+
+
+# ------------------------------------------------- transfers (a8, a9)
+@pytest.mark.parametrize("kind", ALL_KINDS)
+@pytest.mark.parametrize("degree", [0, 1, 2])
+def test_polynomial_reproduction_small(disk_small, kind, degree):
+    # reference test_pointwise.py:146-163 + values vs the reference's
+    polys = {
+        0: lambda x, y: np.full_like(x, 3.5),
+        1: lambda x, y: 2 * x - y + 1,
+        2: lambda x, y: x * x + 2 * x * y - y * y + x + 0.5,
+    }
+    f = sample_field(disk_small, polys[degree])
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(degree, P.RadialBasisSpec(kind, a=2.0),
+                     P.AdaptiveRadius(max(6, 2 * P.n_monomials(degree)), 1.5 * h, 1.5), lam=0.0)
+    got = P.transfer_pointwise(f, disk_small.centroids(), spec)
+    c = disk_small.centroids()
+    want = polys[degree](c[:, 0], c[:, 1])
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-10
+    ref = golden("poly_repro")[f"{kind.value}_{degree}"]
+    assert _rel(got, ref) < VALUE_RTOL
+
+
+def test_cutoff_locality_bitwise(disk_small):
+    h = disk_small.mean_edge_length
+    r_c = 2.0 * h
+    f = sample_field(disk_small, lambda x, y: np.sin(x) * np.cos(y) + 2)
+    targets = disk_small.centroids()[:40]
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(r_c))
+    base = P.transfer_pointwise(f, targets, spec)
+    d = np.linalg.norm(disk_small.coords[None, :, :] - targets[:, None, :], axis=2).min(axis=0)
+    far = int(np.argmax(d))
+    assert d[far] > r_c
+    values = f.values.copy()
+    values[far] += 1e6
+    assert np.array_equal(base, P.transfer_pointwise(f.with_values(values), targets, spec))
+
+
+def test_transfer_against_dense_least_squares_oracle(disk_small):
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2.0 * h))
+    f = sample_field(disk_small, lambda x, y: np.sin(x) * np.cos(y) + 2)
+    targets = disk_small.centroids()
+    got = P.transfer_pointwise(f, targets, spec)
+    src = disk_small.coords
+    oracle = np.empty(targets.shape[0])
+    for i, t in enumerate(targets):
+        d = np.linalg.norm(src - t, axis=1)
+        sel = np.nonzero(d < 2.0 * h)[0]
+        w = O.rbf_weights(O.RBF_C4, 2.0, 2.0 * h, d[sel])
+        A = np.column_stack([np.ones(sel.size), src[sel, 0] - t[0], src[sel, 1] - t[1]])
+        cc, *_ = np.linalg.lstsq(A * w[:, None], w * f.values[sel], rcond=None)
+        oracle[i] = cc[0]
+    assert np.abs(got - oracle).max() < 1e-12
+    assert _rel(got, golden("poly_repro")["fixed_c4_1"]) < VALUE_RTOL
+
+
+def test_transfer_threads_identical(disk_small):
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2.0 * h))
+    f = sample_field(disk_small, lambda x, y: np.sin(3 * x) + y)
+    one = P.transfer_pointwise(f, disk_small.centroids(), spec, threads=1)
+    four = P.transfer_pointwise(f, disk_small.centroids(), spec, threads=4)
+    assert np.array_equal(one, four)
+
+
+def test_extrinsic_analytic_callback_exact(disk_small):
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.GAUSSIAN), P.FixedRadius(2.5 * h))
+    got = P.transfer_extrinsic(lambda p: 4 * p[:, 0] - p[:, 1] + 2, disk_small.centroids(), spec,
+                               disk_small.coords)
+    c = disk_small.centroids()
+    assert np.abs(got - (4 * c[:, 0] - c[:, 1] + 2)).max() < 1e-10
+
+
+def test_extrinsic_matches_intrinsic_bitwise(disk_small):
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2.0 * h))
+    f = sample_field(disk_small, lambda x, y: np.sin(x) * np.cos(y) + 2)
+    table = {(float(x), float(y)): float(v) for (x, y), v in zip(disk_small.coords, f.values)}
+    calls = []
+
+    def callback(pts):
+        calls.append(len(pts))
+        return np.array([table[(float(x), float(y))] for x, y in pts])
+
+    intrinsic = P.transfer_pointwise(f, disk_small.centroids(), spec)
+    extrinsic = P.transfer_extrinsic(callback, disk_small.centroids(), spec, disk_small.coords,
+                                     batch_size=100)
+    assert np.array_equal(intrinsic, extrinsic)
+    assert len(calls) <= int(np.ceil(disk_small.nelems / 100))
+
+
+def test_extrinsic_failure_names_batch(disk_small):
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(0, P.RadialBasisSpec(P.RbfKind.CONST), P.FixedRadius(2.0 * h))
+    state = {"batch": 0}
+
+    def flaky(pts):
+        if state["batch"] == 3:
+            raise RuntimeError("remote evaluation unavailable")
+        state["batch"] += 1
+        return np.zeros(len(pts))
+
+    with pytest.raises(P.ExtrinsicEvaluationError) as exc:
+        P.transfer_extrinsic(flaky, disk_small.centroids(), spec, disk_small.coords,
+                             batch_size=50)
+    assert exc.value.batch == 3 and "batch 3" in str(exc.value)
+
+
+def test_source_equals_target_polynomial_consistency(disk_small):
+    f = sample_field(disk_small, lambda x, y: x - 2 * y + 3)
+    h = disk_small.mean_edge_length
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2.5 * h))
+    got = P.transfer_pointwise(f, disk_small.coords, spec)
+    assert np.linalg.norm(got - f.values) / np.linalg.norm(f.values) < 1e-10
+
+
+def test_c1_values_vs_reference():
+    g = golden("c1")
+    src, tg, vals, h = _c1()
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.FixedRadius(2 * h))
+    got = P.fit_point_cloud(src, vals, tg, spec)
+    assert _rel(got, g["values"]) < VALUE_RTOL
+
+
+def test_prepared_transfer_adaptive_vs_reference():
+    g = golden("adaptive")
+    src = synth.disk_graded(1.0, 30, 0.6).coords
+    tg = synth.disk(1.0, 30).coords
+    h = float(g["mean_edge_length"])
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.AdaptiveRadius(12, h, 1.5))
+    pt = P.PreparedTransfer(src, tg, spec)
+    vals3 = synth.sincos_field(src, 3)
+    Y = pt.apply(vals3)
+    assert Y.shape == (tg.shape[0], 3)
+    assert _rel(Y, g["values3"]) < VALUE_RTOL
+    for c in range(3):
+        assert _rel(pt.apply(vals3[:, c]), g["values3"][:, c]) < VALUE_RTOL
+    off, idx, w = pt.support
+    assert np.array_equal(off, g["off"]) and np.array_equal(idx, g["idx"])
+    with pytest.raises(P.FieldError):
+        pt.apply(np.ones(3))
+
+
+def test_random_cloud_gaussian_multiquadric():
+    g = golden("random_clouds")
+    src, tg = g["src"], g["tg"]
+    vals = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    for kind in (P.RbfKind.GAUSSIAN, P.RbfKind.MULTIQUADRIC):
+        spec = P.FitSpec(2, P.RadialBasisSpec(kind, a=2.0),
+                         P.AdaptiveRadius(12, 1.5 / np.sqrt(src.shape[0]), 1.5))
+        assert _rel(P.fit_point_cloud(src, vals, tg, spec), g[kind.value]) < VALUE_RTOL
+
+
+def test_singular_transfer_raises():
+    # all sources on a line: a degree-1 fit is rank deficient everywhere
+    x = np.linspace(0, 1, 50)
+    src = np.column_stack([x, 0.5 * x])
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.CONST), P.FixedRadius(0.3))
+    with pytest.raises(P.SingularFitError, match="rank-deficient degree-1"):
+        P.fit_point_cloud(src, x, src[10:20], spec)
+    pt = P.PreparedTransfer(src, src[10:20], spec)  # supports fine, fit fails at apply
+    with pytest.raises(P.SingularFitError):
+        pt.apply(x)
+
+
+def test_empty_weight_support_raises_singular():
+    # thin plate spline weight is 0 at r = 0: a lone coincident source has no weight
+    src = np.array([[0.0, 0.0], [5.0, 5.0]])
+    spec = P.FitSpec(0, P.RadialBasisSpec(P.RbfKind.THIN_PLATE_SPLINE), P.FixedRadius(0.5))
+    with pytest.raises(P.SingularFitError, match="no support points with nonzero weight"):
+        P.fit_point_cloud(src, np.ones(2), [(0.0, 0.0)], spec)
+
+
+def test_empty_targets():
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(0.1))
+    src = np.random.RandomState(0).uniform(0, 1, (100, 2))
+    assert P.fit_point_cloud(src, np.ones(100), np.zeros((0, 2)), spec).shape == (0,)
+    off, idx, dist = Kb.fixed_radius_supports(np.zeros((0, 2)), src, 0.0, 0.0, 0.1, 0.1, 10, 10,
+                                              None, None, 0.1)
+    assert off.tolist() == [0] and idx.size == 0
+
+
+# ------------------------------------------------ extensions (oracle)
+def test_extension_3d_degree3_vs_oracle():
+    rng = np.random.RandomState(3)
+    src = rng.uniform(0, 1, (6000, 3))
+    tg = rng.uniform(0.1, 0.9, (500, 3))
+    vals = np.cos(2 * src[:, 0]) + src[:, 1] * src[:, 2]
+    spec = P.FitSpec(3, P.RadialBasisSpec(P.RbfKind.C4), P.AdaptiveRadius(40, 0.05, 1.5))
+    got = P.fit_point_cloud(src, vals, tg, spec)
+    want, st, sup = O.transfer(src, vals, tg, 3, O.RBF_C4, 2.0, ("adaptive", 40, 0.05, 1.5))
+    assert (st == 0).all()
+    assert _rel(got, want) < VALUE_RTOL
+
+
+@pytest.mark.parametrize("dim,deg", [(1, 2), (3, 2), (4, 1), (5, 1), (5, 2)])
+def test_extension_nd_vs_oracle(dim, deg):
+    rng = np.random.RandomState(10 + dim)
+    ns = {1: 500, 3: 8000, 4: 20000, 5: 30000}[dim]
+    src = rng.uniform(0, 1, (ns, dim))
+    tg = rng.uniform(0.2, 0.8, (300, dim))
+    vals = np.sin(src.sum(axis=1)) + 2
+    need = P.n_monomials(deg, dim)
+    spec = P.FitSpec(deg, P.RadialBasisSpec(P.RbfKind.C4), P.AdaptiveRadius(2 * need, 0.02, 1.5))
+    got = P.fit_point_cloud(src, vals, tg, spec)
+    want, st, _ = O.transfer(src, vals, tg, deg, O.RBF_C4, 2.0, ("adaptive", 2 * need, 0.02, 1.5))
+    assert (st == 0).all()
+    assert _rel(got, want) < VALUE_RTOL
+
+
+def test_extension_multicomponent_apply_equals_columns():
+    src, tg, vals, h = _c1()
+    V = synth.sincos_field(src, 8)
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2 * h))
+    pt = P.PreparedTransfer(src, tg, spec)
+    Y = pt.apply(V)
+    want, _c, st = O.fit_many_nd(tg, *O.supports_nd(tg, O.OraclePointGrid(src), 2 * h)[:2],
+                                 np.abs(O.rbf_weights(O.RBF_C4, 2.0, 2 * h,
+                                                      O.supports_nd(tg, O.OraclePointGrid(src),
+                                                                    2 * h)[2])),
+                                 src, V, 2, 0.0, True)
+    assert _rel(Y, want) < VALUE_RTOL
+    assert _rel(P.fit_point_cloud(src, V, tg, spec), want) < VALUE_RTOL
