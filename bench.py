@@ -90,22 +90,36 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.timed_from = 0
+        self.err = ""
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
-        except OSError:
+        except OSError as exc:
             self.proc = None
+            self.err = str(exc)
         return self
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first_sample(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            if self.proc.poll() is not None:
+                self.err = (self.proc.stderr.read() or "")[-300:]
+                break
+            time.sleep(0.02)
+
+    def mark_timed(self):
+        self.timed_from = len(self.lines)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -118,7 +132,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples from the timed region (plus the last warm-up sample when the
+        # timed region is shorter than the sampling period)
+        lines = self.lines[max(0, self.timed_from - 1):]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -130,8 +147,11 @@ class ClockSampler:
             for n, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if not sm and self.err:
+            out["error"] = self.err
+        return out
 
 
 def measured_peaks():
@@ -151,8 +171,9 @@ def fit_flops(counts, k):
 # ------------------------------------------------------------ b200 arm
 # kernels launched by one device step (our own, counted from the launch
 # sequence in device.py / libfieldmap.so): source bbox 3, grid build 7,
-# target order 5, r_max bboxes 6, count 2, scan 3, operator build 2, apply 1
-LAUNCHES_PER_STEP = 3 + 7 + 5 + 6 + 2 + 3 + 2 + 1
+# target order 5, target bbox 3, select 2, ordered offsets 4, operator build 2,
+# apply 1 (+1 build launch per step if some support overflows its slot)
+LAUNCHES_PER_STEP = 3 + 7 + 5 + 3 + 2 + 4 + 2 + 1
 
 
 def b200_step(src_d, tgt_d, X_d, spec, marks):
@@ -173,12 +194,12 @@ def b200_step(src_d, tgt_d, X_d, spec, marks):
     perm = cloud.target_order(tgt_d)
     mark("order")
     sel = spec.selection
-    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, _r_max_device(cloud.pts, tgt_d)) \
+    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, _r_max_device(cloud, tgt_d)) \
         if hasattr(sel, "min_points") else D.fixed(sel.r_c)
-    cnt = D.count_supports(cloud, tgt_d, dsel, perm, 0)
-    mark("count")
-    op, stats = D.build_operator(cloud, tgt_d, dsel, cnt, P._rbf_pair(spec.rbf), spec.degree,
-                                 spec.lam, spec.centering, perm)
+    cnt = D.select(cloud, tgt_d, dsel, perm, 0)
+    mark("select")
+    op, stats = D.build_operator(cloud, tgt_d, cnt, P._rbf_pair(spec.rbf), spec.degree, spec.lam,
+                                 spec.centering)
     mark("build")
     Y = op.apply(X_d)
     mark("apply")
@@ -208,18 +229,20 @@ def run_b200(args, rank, world, local_rank):
             marks.append(("allgather", e))
         return Y, op, cnt, stats
 
-    for _ in range(args.warmup):
-        Y, op, cnt, stats = step([])
-    torch.cuda.synchronize()
-    if int(stats[0].item()) != 0:
-        raise SystemExit(f"{int(stats[0].item())} fits failed in the benchmark workload")
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    phase = {}
-    step_ms = []
     sampler = ClockSampler(local_rank)
     with sampler:
+        sampler.wait_first_sample()
+        for _ in range(args.warmup):
+            Y, op, cnt, stats = step([])
+        torch.cuda.synchronize()
+        if int(stats[0].item()) != 0:
+            raise SystemExit(f"{int(stats[0].item())} fits failed in the benchmark workload")
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        phase = {}
+        step_ms = []
+        sampler.mark_timed()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             marks = []
@@ -299,7 +322,7 @@ def run_b200(args, rank, world, local_rank):
         "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "roofline": {
-            "kernel": "k_fused_fit (fused fill + C4 weights + Householder QR + operator row)",
+            "kernel": "k_build (C4 weights + Householder QR + operator row, supports from k_select)",
             "bound": "fp64",
             "achieved": flops / (build_ms * 1e-3) / 1e12,
             "peak": fp64_peak,
@@ -429,7 +452,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=["c1", "c2"], default="c2")

@@ -184,39 +184,79 @@ int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int6
                 const double *src_val, double *values, double *coeffs, uint8_t *status,
                 int32_t *stats, fm_stream_t stream);
 
+/* ----------------------------- a3/a4 + lists: the select pass (new)
+ * Count pass that also emits every target's support, sorted by source id
+ * (the order of _sort_by_id, _ext.pyx:155-169), into a fixed-stride slot
+ * buffer indexed by PROCESSING POSITION k (the k-th entry of perm):
+ * slot_id/slot_pos[k*slot_cap + i] = source id / index into sorted_pts.
+ * counts/radii/status are indexed by target and equal fm_support_count's.
+ * Adaptive selection evaluates several radii of the reference's growth
+ * sequence per window scan (first scan at a density-guessed step) -- the
+ * chosen radius is still the first of that exact sequence holding min_pts.
+ * Targets whose support exceeds slot_cap are appended (as positions k) to
+ * overflow[]; the build re-gathers them.  stats (device int32[8], written
+ * by the call): fm_support_count's 6 entries, [6] #overflow, [7] 0. */
+int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+                       const int32_t *sorted_ids, const double *targets, int64_t nt,
+                       const int32_t *perm, const fm_select *sel, int32_t min_required,
+                       int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
+                       int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
+                       fm_stream_t stream);
+
+/* Row offsets of an operator stored in processing order:
+ * offsets[k+1] = offsets[k] + counts[perm[k]] (perm may be NULL). */
+size_t fm_offsets_ordered_workspace(int64_t n);
+int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int64_t *offsets,
+                       void *workspace, size_t workspace_bytes, fm_stream_t stream);
+
+/* Supports produced by fm_select (device pointers; n_overflow is the host
+ * copy of stats[6]). */
+typedef struct fm_lists {
+    const int32_t *counts;
+    const int32_t *slot_id;
+    const int32_t *slot_pos;
+    int32_t slot_cap;
+    int32_t n_overflow;
+    const int32_t *overflow;
+} fm_lists;
+
 /* --------------------------------- a8/a13: transfer operator (new)
- * Fused fill + weights + fit producing the explicit transfer operator
- * W (nt x ns, CSR rows at offsets, ids ascending): row t holds
- * W[t, j] = e_t^T (the value functional of the reference's fit) so that
- * W @ f reproduces fit_many's `values` for every field f (the fit is linear
- * in src_val, _ext.pyx:394).  col[nnz] = source id, val[nnz] = weight
- * (NaN row on failure), status[nt] and stats[2] as fit_many.  This is what
+ * Weights + fit producing the explicit transfer operator W (nt x ns) whose
+ * rows are stored in PROCESSING ORDER: stored row k (target perm[k]) spans
+ * [offsets[k], offsets[k+1]) with source ids ascending, so that W @ f
+ * reproduces fit_many's `values` for every field f (the fit is linear in
+ * src_val, _ext.pyx:394).  col[nnz] = source id, val[nnz] = weight (NaN row
+ * on failure), status[nt] (by target) and stats[2] as fit_many.  With
+ * `lists` (from fm_select) the supports are read from the slots and only
+ * overflow targets are re-gathered; with lists == NULL every support is
+ * re-gathered (max_count >= every support size).  This is what
  * PreparedTransfer (pointwise.py:399-431) caches instead of the raw support. */
 int fm_build_operator(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                       const int32_t *sorted_ids, const double *targets, int64_t nt,
                       const int32_t *perm, const fm_select *sel, const double *radii,
-                      const int64_t *offsets, int32_t max_count, const fm_rbf *rbf,
-                      const fm_fit *fit, const double *src, int32_t *col, double *val,
+                      const fm_lists *lists, const int64_t *offsets, int32_t max_count,
+                      const fm_rbf *rbf, const fm_fit *fit, int32_t *col, double *val,
                       uint8_t *status, int32_t *stats, fm_stream_t stream);
 
-/* One-shot fused transfer of a scalar field (fit_point_cloud,
- * pointwise.py:434-451): fill + weights + fit_many per target without
- * materialising supports.  values[nt] (NaN on failure), status[nt],
- * stats[2] as fit_many. */
+/* One-shot transfer of a scalar field (fit_point_cloud, pointwise.py:434-451):
+ * weights + fit_many per target straight from the supports (lists, or
+ * re-gathered when lists == NULL) without materialising the operator.
+ * values[nt] (NaN on failure), status[nt], stats[2] as fit_many. */
 int fm_transfer_values(const fm_grid *grid, const int32_t *cell_start,
                        const double *sorted_pts, const int32_t *sorted_ids,
                        const double *targets, int64_t nt, const int32_t *perm,
-                       const fm_select *sel, const double *radii, int32_t max_count,
-                       const fm_rbf *rbf, const fm_fit *fit, const double *src,
+                       const fm_select *sel, const double *radii, const fm_lists *lists,
+                       int32_t max_count, const fm_rbf *rbf, const fm_fit *fit,
                        const double *src_val, double *values, uint8_t *status,
                        int32_t *stats, fm_stream_t stream);
 
-/* Apply the operator to a multi-component field: Y[t, :] = sum_j
- * val[j] * X[col[j], :] over row t (PreparedTransfer.apply,
- * pointwise.py:418-431, without re-solving).  X (ns, ncomp), Y (nt, ncomp)
- * row-major.  row_order (may be NULL) is the processing order (perm). */
-int fm_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const double *val,
-             const int32_t *row_order, const double *X, int32_t ncomp, double *Y,
+/* Apply the operator to a multi-component field (PreparedTransfer.apply,
+ * pointwise.py:418-431, without re-solving): for every stored row k,
+ * Y[row_target[k], :] = sum_j val[j] * X[col[j], :] over [row_off[k],
+ * row_off[k+1]).  X (ns, ncomp), Y (nrows, ncomp) row-major; row_target
+ * (may be NULL: identity) is the perm the operator was built with. */
+int fm_apply(int64_t nrows, const int64_t *row_off, const int32_t *col, const double *val,
+             const int32_t *row_target, const double *X, int32_t ncomp, double *Y,
              fm_stream_t stream);
 
 /* ---------------------------------------------------- measurement

@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "fm_kernels.cuh"
+#include "fm_scan.cuh"
 
 namespace fm {
 
@@ -16,97 +17,121 @@ __global__ void k_rbf(int kind, double a, double r_c, const double *__restrict__
 }
 
 // -------------------------------------------------------------- apply
-// Y[t, :] = sum_j val[j] * X[col[j], :] over the CSR row of t.  L lanes per
-// row, V consecutive components per lane (C = L*V), rows visited in
-// `order` (cell order) so that the X rows gathered by neighbouring rows are
-// shared through L1/L2.  4-way unrolled over the nonzeros so each lane has
-// several independent gathers in flight.
+// Y[row_target[k], :] = sum_j val[j] * X[col[j], :] over stored row k.
+// Rows are stored in processing (cell) order, so a warp's tile of 32/L
+// consecutive rows is one contiguous nnz range: the warp stages its
+// (col, val) stream through shared memory with coalesced loads, then each
+// row group of L lanes (V consecutive components per lane, C = L*V) gathers
+// the X rows -- one 16-byte load per lane per nonzero, 8 in flight.
+constexpr int kApplyChunk = 256;  // staged nonzeros per warp and pass
+
 template <int L, int V>
-__global__ void __launch_bounds__(256) k_apply(int64_t nt, const int64_t *__restrict__ row_off,
+__global__ void __launch_bounds__(256) k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
                                                const int32_t *__restrict__ col,
                                                const double *__restrict__ val,
-                                               const int32_t *__restrict__ order,
+                                               const int32_t *__restrict__ row_target,
                                                const double *__restrict__ X,
                                                double *__restrict__ Y) {
     constexpr int C = L * V;
-    const int64_t slot0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L;
-    const int li = threadIdx.x % L;
-    const int64_t nslots = ((int64_t)gridDim.x * blockDim.x) / L;
-    for (int64_t r = slot0; r < nt; r += nslots) {
-        const int64_t t = order ? (int64_t)order[r] : r;
-        const int64_t b = row_off[t], e = row_off[t + 1];
+    constexpr int RPW = 32 / L;
+    constexpr int U = 8;
+    __shared__ int32_t s_col[8][kApplyChunk];
+    __shared__ double s_val[8][kApplyChunk];
+    const int wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int rr = lane / L, li = lane % L;
+    int32_t *sc = s_col[wib];
+    double *sv = s_val[wib];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t tile = warp; tile * RPW < nrows; tile += nwarps) {
+        const int64_t r0 = tile * RPW;
+        const int64_t rend = r0 + RPW < nrows ? r0 + RPW : nrows;
+        const int64_t r = r0 + rr;
+        const bool active = r < nrows;
+        const int64_t rb = active ? __ldg(row_off + r) : 0;
+        const int64_t re = active ? __ldg(row_off + r + 1) : 0;
+        const int64_t tb = __ldg(row_off + r0), te = __ldg(row_off + rend);
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = 0.0;
-        int64_t j = b;
-        for (; j + 4 <= e; j += 4) {
-            int32_t c4[4];
-            double w4[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                c4[u] = __ldg(col + j + u);
-                w4[u] = __ldg(val + j + u);
+        for (int64_t cs = tb; cs < te; cs += kApplyChunk) {
+            const int n = (int)(te - cs < kApplyChunk ? te - cs : kApplyChunk);
+            for (int i = lane; i < n; i += 32) {
+                sc[i] = __ldg(col + cs + i);
+                sv[i] = __ldg(val + cs + i);
             }
-            double x4[4][V];
+            __syncwarp();
+            const int j0 = (int)((rb > cs ? rb : cs) - cs);
+            const int j1 = (int)((re < cs + n ? re : cs + n) - cs);
+            int j = j0;
+            for (; j + U <= j1; j += U) {
+                double x[U][V];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const double *xp = X + (int64_t)c4[u] * C + li * V;
-                if (V == 2) {
-                    const double2 x2 = __ldg(reinterpret_cast<const double2 *>(xp));
-                    x4[u][0] = x2.x;
-                    x4[u][V - 1] = x2.y;
-                } else {
+                for (int u = 0; u < U; u++) {
+                    const double *xp = X + (int64_t)sc[j + u] * C + li * V;
+                    if (V == 2) {
+                        const double2 x2 = __ldg(reinterpret_cast<const double2 *>(xp));
+                        x[u][0] = x2.x;
+                        x[u][V - 1] = x2.y;
+                    } else {
 #pragma unroll
-                    for (int v = 0; v < V; v++) x4[u][v] = __ldg(xp + v);
+                        for (int v = 0; v < V; v++) x[u][v] = __ldg(xp + v);
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int v = 0; v < V; v++) acc[v] = fma(sv[j + u], x[u][v], acc[v]);
             }
+            for (; j < j1; j++) {
+                const double *xp = X + (int64_t)sc[j] * C + li * V;
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-#pragma unroll
-                for (int v = 0; v < V; v++) acc[v] = fma(w4[u], x4[u][v], acc[v]);
+                for (int v = 0; v < V; v++) acc[v] = fma(sv[j], __ldg(xp + v), acc[v]);
+            }
+            __syncwarp();
         }
-        for (; j < e; j++) {
-            const int32_t c = __ldg(col + j);
-            const double w = __ldg(val + j);
-            const double *xp = X + (int64_t)c * C + li * V;
+        if (active) {
+            const int64_t t = row_target ? (int64_t)row_target[r] : r;
+            double *yp = Y + t * C + li * V;
+            if (V == 2) {
+                *reinterpret_cast<double2 *>(yp) = make_double2(acc[0], acc[V - 1]);
+            } else {
 #pragma unroll
-            for (int v = 0; v < V; v++) acc[v] = fma(w, __ldg(xp + v), acc[v]);
-        }
-        double *yp = Y + t * C + li * V;
-        if (V == 2) {
-            *reinterpret_cast<double2 *>(yp) = make_double2(acc[0], acc[V - 1]);
-        } else {
-#pragma unroll
-            for (int v = 0; v < V; v++) yp[v] = acc[v];
+                for (int v = 0; v < V; v++) yp[v] = acc[v];
+            }
         }
     }
 }
 
-// any C: one thread per (row, component)
-__global__ void k_apply_generic(int64_t nt, const int64_t *__restrict__ row_off,
+// any C: one thread per (stored row, component)
+__global__ void k_apply_generic(int64_t nrows, const int64_t *__restrict__ row_off,
                                 const int32_t *__restrict__ col, const double *__restrict__ val,
-                                const int32_t *__restrict__ order, const double *__restrict__ X,
-                                int C, double *__restrict__ Y) {
-    const int64_t total = nt * C;
+                                const int32_t *__restrict__ row_target,
+                                const double *__restrict__ X, int C, double *__restrict__ Y) {
+    const int64_t total = nrows * C;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = g / C;
         const int c = (int)(g % C);
-        const int64_t t = order ? (int64_t)order[r] : r;
         double acc = 0.0;
-        for (int64_t j = row_off[t]; j < row_off[t + 1]; j++)
+        for (int64_t j = row_off[r]; j < row_off[r + 1]; j++)
             acc = fma(__ldg(val + j), __ldg(X + (int64_t)__ldg(col + j) * C + c), acc);
+        const int64_t t = row_target ? (int64_t)row_target[r] : r;
         Y[t * C + c] = acc;
     }
 }
 
 template <int L, int V>
-static int launch_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const double *val,
-                        const int32_t *order, const double *X, double *Y, cudaStream_t st) {
+static int launch_apply(int64_t nrows, const int64_t *row_off, const int32_t *col,
+                        const double *val, const int32_t *row_target, const double *X, double *Y,
+                        cudaStream_t st) {
     const int threads = 256;
-    const int64_t need = (nt * L + threads - 1) / threads;
+    constexpr int RPW = 32 / L;
+    const int64_t tiles = (nrows + RPW - 1) / RPW;
+    const int64_t need = (tiles + 7) / 8;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kSMs * 8));
-    k_apply<L, V><<<blocks, threads, 0, st>>>(nt, row_off, col, val, order, X, Y);
+    k_apply<L, V><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -261,62 +286,138 @@ int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int6
     return FM_ERR_UNSUPPORTED;
 }
 
-static int fused_common(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+static int dispatch_build(int dim, int degree, bool solve, bool slots, const SearchArgs &s,
+                          const BuildArgs &b, int max_m, cudaStream_t st) {
+#define FM_BUILD_CASE(N, P) \
+    case N * 10 + P: return dim##N##_deg##P##_build(solve, slots, s, b, max_m, st);
+    switch (dim * 10 + degree) {
+        FM_BUILD_CASE(1, 0) FM_BUILD_CASE(1, 1) FM_BUILD_CASE(1, 2) FM_BUILD_CASE(1, 3)
+        FM_BUILD_CASE(2, 0) FM_BUILD_CASE(2, 1) FM_BUILD_CASE(2, 2) FM_BUILD_CASE(2, 3)
+        FM_BUILD_CASE(3, 0) FM_BUILD_CASE(3, 1) FM_BUILD_CASE(3, 2) FM_BUILD_CASE(3, 3)
+        FM_BUILD_CASE(4, 0) FM_BUILD_CASE(4, 1) FM_BUILD_CASE(4, 2)
+        FM_BUILD_CASE(5, 0) FM_BUILD_CASE(5, 1) FM_BUILD_CASE(5, 2)
+    }
+#undef FM_BUILD_CASE
+    return FM_ERR_UNSUPPORTED;
+}
+
+static int build_common(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                         const int32_t *sorted_ids, const double *targets, int64_t nt,
                         const int32_t *perm, const fm_select *sel, const double *radii,
-                        const int64_t *offsets, int32_t max_count, const fm_rbf *rbf,
-                        const fm_fit *fit, const double *src, const double *src_val,
+                        const fm_lists *lists, const int64_t *offsets, int32_t max_count,
+                        const fm_rbf *rbf, const fm_fit *fit, const double *src_val,
                         int32_t *col, double *val, double *values, uint8_t *status,
                         int32_t *stats, bool solve, fm_stream_t stream) {
     if (!grid_ok(grid) || !sel || !rbf || nt < 0 || max_count < 0) return FM_ERR_ARG;
     if (!fit_ok(fit)) return fit && fit->degree <= 3 ? FM_ERR_UNSUPPORTED : FM_ERR_ARG;
     if (fit->dim != grid->dim || rbf->kind < 0 || rbf->kind > 7) return FM_ERR_ARG;
     if (sel->adaptive && !radii) return FM_ERR_ARG;
+    if (lists && (!lists->counts || !lists->slot_id || !lists->slot_pos || lists->slot_cap < 1 ||
+                  lists->n_overflow < 0 || (lists->n_overflow > 0 && !lists->overflow)))
+        return FM_ERR_ARG;
     const SearchArgs s = make_search(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm,
                                      sel, sel->adaptive ? radii : nullptr);
     cudaStream_t st = (cudaStream_t)stream;
-#define FM_FUSED_CASE(N, P)                                                                  \
-    case N * 10 + P:                                                                         \
-        return dim##N##_deg##P##_fused(solve, s, offsets, max_count, *rbf, *fit, src,       \
-                                       src_val, col, val, values, status, stats, st);
-    switch (grid->dim * 10 + fit->degree) {
-        FM_FUSED_CASE(1, 0) FM_FUSED_CASE(1, 1) FM_FUSED_CASE(1, 2) FM_FUSED_CASE(1, 3)
-        FM_FUSED_CASE(2, 0) FM_FUSED_CASE(2, 1) FM_FUSED_CASE(2, 2) FM_FUSED_CASE(2, 3)
-        FM_FUSED_CASE(3, 0) FM_FUSED_CASE(3, 1) FM_FUSED_CASE(3, 2) FM_FUSED_CASE(3, 3)
-        FM_FUSED_CASE(4, 0) FM_FUSED_CASE(4, 1) FM_FUSED_CASE(4, 2)
-        FM_FUSED_CASE(5, 0) FM_FUSED_CASE(5, 1) FM_FUSED_CASE(5, 2)
+    if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 2, 1);
+    BuildArgs b{};
+    b.nk = nt;
+    b.offsets = offsets;
+    b.cap = max_count < 1 ? 1 : max_count;
+    b.rbf_kind = rbf->kind;
+    b.rbf_a = rbf->a;
+    b.fp = *fit;
+    b.src_val = src_val;
+    b.col = col;
+    b.val = val;
+    b.values = values;
+    b.status = status;
+    b.stats = stats;
+    int rc;
+    if (lists) {
+        b.slot_id = lists->slot_id;
+        b.slot_pos = lists->slot_pos;
+        b.slot_cap = lists->slot_cap;
+        b.counts = lists->counts;
+        const int mm = max_count < lists->slot_cap ? max_count : lists->slot_cap;
+        rc = dispatch_build(grid->dim, fit->degree, solve, true, s, b, mm, st);
+        if (rc || lists->n_overflow == 0) return rc;
+        b.klist = lists->overflow;
+        b.nk = lists->n_overflow;
     }
-#undef FM_FUSED_CASE
-    return FM_ERR_UNSUPPORTED;
+    return dispatch_build(grid->dim, fit->degree, solve, false, s, b, b.cap, st);
 }
 
 int fm_build_operator(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                       const int32_t *sorted_ids, const double *targets, int64_t nt,
                       const int32_t *perm, const fm_select *sel, const double *radii,
-                      const int64_t *offsets, int32_t max_count, const fm_rbf *rbf,
-                      const fm_fit *fit, const double *src, int32_t *col, double *val,
+                      const fm_lists *lists, const int64_t *offsets, int32_t max_count,
+                      const fm_rbf *rbf, const fm_fit *fit, int32_t *col, double *val,
                       uint8_t *status, int32_t *stats, fm_stream_t stream) {
     if (!offsets || !col || !val || !status) return FM_ERR_ARG;
-    return fused_common(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel, radii,
-                        offsets, max_count, rbf, fit, src, nullptr, col, val, nullptr, status,
+    return build_common(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel, radii,
+                        lists, offsets, max_count, rbf, fit, nullptr, col, val, nullptr, status,
                         stats, false, stream);
 }
 
 int fm_transfer_values(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                        const int32_t *sorted_ids, const double *targets, int64_t nt,
                        const int32_t *perm, const fm_select *sel, const double *radii,
-                       int32_t max_count, const fm_rbf *rbf, const fm_fit *fit,
-                       const double *src, const double *src_val, double *values,
-                       uint8_t *status, int32_t *stats, fm_stream_t stream) {
+                       const fm_lists *lists, int32_t max_count, const fm_rbf *rbf,
+                       const fm_fit *fit, const double *src_val, double *values, uint8_t *status,
+                       int32_t *stats, fm_stream_t stream) {
     if (!src_val || !values || !status) return FM_ERR_ARG;
-    return fused_common(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel, radii,
-                        nullptr, max_count, rbf, fit, src, src_val, nullptr, nullptr, values,
+    return build_common(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel, radii,
+                        lists, nullptr, max_count, rbf, fit, src_val, nullptr, nullptr, values,
                         status, stats, true, stream);
 }
 
+int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+                       const int32_t *sorted_ids, const double *targets, int64_t nt,
+                       const int32_t *perm, const fm_select *sel, int32_t min_required,
+                       int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
+                       int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
+                       fm_stream_t stream) {
+    if (!grid_ok(grid) || !sel || nt < 0 || slot_cap < 1 || !stats || !overflow || !counts)
+        return FM_ERR_ARG;
+    if (sel->adaptive ? !(sel->r0 > 0.0 && sel->growth > 1.0 && sel->min_pts >= 1 && radii)
+                      : !(sel->r_c > 0.0))
+        return FM_ERR_ARG;
+    const SearchArgs s = make_search(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm,
+                                     sel, nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (grid->dim) {
+    case 1: return dim1_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    case 2: return dim2_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    case 3: return dim3_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    case 4: return dim4_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    default: return dim5_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    }
+}
+
+size_t fm_offsets_ordered_workspace(int64_t n) {
+    return align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)) + scan_workspace_bytes(n);
+}
+
+int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int64_t *offsets,
+                       void *workspace, size_t workspace_bytes, fm_stream_t stream) {
+    if (n < 0) return FM_ERR_ARG;
+    if (workspace_bytes < fm_offsets_ordered_workspace(n)) return FM_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t *tmp = reinterpret_cast<int32_t *>(workspace);
+    char *scan_ws = reinterpret_cast<char *>(workspace) +
+                    align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    if (n > 0) {
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
+        k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, tmp);
+        FM_CHECK_LAUNCH();
+    }
+    return exclusive_scan<int32_t, int64_t>(tmp, n, offsets, scan_ws, scan_workspace_bytes(n), st);
+}
+
 int fm_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const double *val,
-             const int32_t *row_order, const double *X, int32_t ncomp, double *Y,
+             const int32_t *row_target, const double *X, int32_t ncomp, double *Y,
              fm_stream_t stream) {
+    const int32_t *row_order = row_target;
     if (nt < 0 || ncomp < 1) return FM_ERR_ARG;
     if (nt == 0) return FM_OK;
     cudaStream_t st = (cudaStream_t)stream;

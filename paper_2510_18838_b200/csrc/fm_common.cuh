@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <math.h>
+#include <type_traits>
 #include <stdint.h>
 
 #include "../../include/fieldmap.h"
@@ -177,6 +178,35 @@ __device__ __forceinline__ void eval_monos(const double *x, double *mono) {
             mono[c] = x[M.var[c]];
         else
             mono[c] = mul_rn(mono[M.parent[c]], x[M.var[c]]);
+    }
+}
+
+// 1/x and 1/sqrt(x) to ~1 ulp: MUFU seed + three Newton steps.  Only the fit
+// uses them (held to 1e-10, not bitwise); 0 -> NaN/inf propagates into the
+// rank test, which then reports FIT_SINGULAR.
+__device__ __forceinline__ double rcp_fast(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int it = 0; it < 3; it++) y = fma(y, fma(-x, y, 1.0), y);
+    return y;
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int it = 0; it < 3; it++) y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    return y;
+}
+
+// Compile-time loop: f(std::integral_constant<int, 0>) ... f(<N-1>).  Used
+// where `#pragma unroll` is not honoured and a runtime index would push the
+// register-resident matrix into local memory.
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
     }
 }
 

@@ -6,18 +6,19 @@
 // sqrt(lam)/s^deg when lam > 0, solve min ||A c - b|| and map back
 // c /= s^deg.  value = c[0] (centered) or mono(t) . c.
 //
-// B200 formulation.  One group of G lanes (G = 16 for k <= 10, 32 above)
-// owns one target; lane l holds rows l, l+G, ... (ROWS per lane) of A in
-// registers, zero-padded -- a zero row changes neither R nor Q^T b.  The
-// solve is an unpivoted Householder QR (LAPACK dlarfg convention) whose
-// column norms and reflector dot products are butterfly reductions over the
-// group (identical result on every lane).  Instead of LAPACK dgelsy's
-// column-pivoted QR + incremental condition estimate, rank deficiency is
-// declared when kappa_1(R) = ||R||_1 ||R^-1||_1 >= 1.5/eps (calibrated
-// against dgelsy; the status differs from the reference only for
-// cond(A) within a factor ~2 of 1/eps).  For a well-posed
-// fit the least-squares solution is unique, so values agree with the
-// reference to ~1e-14 relative.
+// B200 formulation.  One group of G lanes owns one target (G = 8 for k <= 6,
+// 16 for k <= 10, 32 up to k = 21: the rank test needs one lane per column);
+// lane l holds rows l, l+G, ... (ROWS per lane) of A in registers,
+// zero-padded -- a zero row changes neither R nor Q^T b.  The solve is an
+// unpivoted Householder QR with unnormalised reflectors v = x - beta e_j,
+// H = I - gamma v v^T, gamma = 1/(|x|(|x| + |x_0|)) (one division per
+// column); column norms and reflector dot products are butterfly reductions
+// over the group (bitwise identical on every lane).  Instead of LAPACK
+// dgelsy's column-pivoted QR + incremental condition estimate, rank
+// deficiency is declared when kappa_1(R) = ||R||_1 ||R^-1||_1 >= 1.5/eps
+// (calibrated against dgelsy; status differs only for cond(A) within a
+// factor ~2 of 1/eps).  For a well-posed fit the LS solution
+// is unique, so values agree with the reference to ~eps*cond(A).
 //
 // Two outputs:
 //   SOLVE  (fit_many):  Q^T b rides along as column k; c = R^-1 (Q^T b).
@@ -36,7 +37,7 @@ constexpr double kSingularKappa = 1.5 / 2.220446049250313e-16;
 template <int DIM, int DEG>
 struct FitShape {
     static constexpr int K = Monos<DIM, DEG>::K;
-    static constexpr int G = K <= 10 ? 16 : 32;
+    static constexpr int G = K <= 6 ? 8 : (K <= 10 ? 16 : 32);
 };
 
 // Returns the group-uniform status (FM_FIT_*).
@@ -55,7 +56,9 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     constexpr Monos<DIM, DEG> M{};
     constexpr int K = Monos<DIM, DEG>::K;
     constexpr int NC = K + (SOLVE ? 1 : 0);
+    static_assert(G >= K, "the rank test assigns one lane per column");
     const int gbase = lane & ~(G - 1);
+    const bool centering = fp.centering != 0;
 
     // ---- EMPTY: no rows, or no positive weight (_ext.pyx:340-350)
     int npos = 0;
@@ -66,11 +69,20 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 
     // ---- support scale s = sqrt(max |dx|^2) (_ext.pyx:353-366)
     double dx[ROWS][DIM];
+    if (centering) {
+#pragma unroll
+        for (int q = 0; q < ROWS; q++)
+#pragma unroll
+            for (int a = 0; a < DIM; a++) dx[q][a] = sub_rn(p[q][a], t[a]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < ROWS; q++)
+#pragma unroll
+            for (int a = 0; a < DIM; a++) dx[q][a] = p[q][a];
+    }
     double smax_l = 0.0;
 #pragma unroll
     for (int q = 0; q < ROWS; q++) {
-#pragma unroll
-        for (int a = 0; a < DIM; a++) dx[q][a] = fp.centering ? sub_rn(p[q][a], t[a]) : p[q][a];
         double d2 = mul_rn(dx[q][0], dx[q][0]);
 #pragma unroll
         for (int a = 1; a < DIM; a++) d2 = add_rn(d2, mul_rn(dx[q][a], dx[q][a]));
@@ -78,6 +90,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     }
     double s = __dsqrt_rn(group_max<G>(smax_l));
     if (s == 0.0) s = 1.0;
+    const double inv_s = 1.0 / s;
     double spow[K];
 #pragma unroll
     for (int c = 0; c < K; c++)
@@ -86,36 +99,46 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
                   : M.deg[c] == 2 ? mul_rn(s, s)
                                   : mul_rn(mul_rn(s, s), s);
 
-    // ---- weighted scaled Vandermonde rows (+ ridge rows), _ext.pyx:374-400
-    const bool ridge = fp.lam > 0.0;
-    const double sqrt_lam = ridge ? sqrt(fp.lam) : 0.0;
+    // ---- weighted scaled Vandermonde rows (_ext.pyx:374-394)
     double A[ROWS][NC];
 #pragma unroll
     for (int q = 0; q < ROWS; q++) {
-        const int i = q * G + glane;
         if (valid[q]) {
             double u[DIM], mono[K];
+            // u = dx / s as a product with 1/s: <= 1 ulp from the reference's
+            // quotient, far below the 1e-10 value tolerance
 #pragma unroll
-            for (int a = 0; a < DIM; a++) u[a] = __ddiv_rn(dx[q][a], s);
+            for (int a = 0; a < DIM; a++) u[a] = dx[q][a] * inv_s;
             eval_monos<DIM, DEG>(u, mono);
             A[q][0] = w[q];
 #pragma unroll
             for (int c = 1; c < K; c++) A[q][c] = mul_rn(mono[c], w[q]);
             if (SOLVE) A[q][NC - 1] = mul_rn(w[q], f[q]);
         } else {
-            const int col = i - m;
-            const bool rrow = ridge && col >= 0 && col < K;
 #pragma unroll
-            for (int c = 0; c < NC; c++)
-                A[q][c] = (rrow && c == col && c < K) ? __ddiv_rn(sqrt_lam, spow[c < K ? c : 0])
-                                                      : 0.0;
+            for (int c = 0; c < NC; c++) A[q][c] = 0.0;
+        }
+    }
+    // ridge rows m .. m+K-1: sqrt(lam) / s^deg on the diagonal (_ext.pyx:395-400)
+    const bool ridge = fp.lam > 0.0;
+    if (ridge) {
+        const double sl = sqrt(fp.lam);
+        double rdiag[K];
+#pragma unroll
+        for (int c = 0; c < K; c++) rdiag[c] = __ddiv_rn(sl, spow[c]);
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) {
+            const int col = q * G + glane - m;
+#pragma unroll
+            for (int c = 0; c < K; c++)
+                if (c == col) A[q][c] = rdiag[c];
         }
     }
 
     // ---- Householder QR, column by column
-    double tau[K], beta[K];
-#pragma unroll
-    for (int j = 0; j < K; j++) {
+    double gam[K], beta[K], inv_beta[K], v0[K];
+    static_for<0, K>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
         const double x0 = __shfl_sync(FM_FULL_MASK, A[j / G][j], gbase + (j % G));
         double sl = 0.0;
 #pragma unroll
@@ -124,25 +147,25 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             if (i > j) sl = fma(A[q][j], A[q][j], sl);
         }
         const double sigma = group_sum<G>(sl);
-        double tj, bj, scal;
+        double gj, bj, vj, ib;
         if (sigma == 0.0) {
-            tj = 0.0;
+            gj = 0.0;  // H = I
             bj = x0;
-            scal = 0.0;
+            vj = 0.0;
+            ib = rcp_fast(x0);
         } else {
-            const double nrm = sqrt(fma(x0, x0, sigma));
+            const double s2 = fma(x0, x0, sigma);
+            const double rn = rsqrt_fast(s2);
+            const double nrm = s2 * rn;
             bj = x0 >= 0.0 ? -nrm : nrm;
-            tj = (bj - x0) / bj;
-            scal = 1.0 / (x0 - bj);
+            ib = x0 >= 0.0 ? -rn : rn;
+            vj = x0 - bj;
+            gj = rcp_fast(nrm * (nrm + fabs(x0)));
         }
-        tau[j] = tj;
+        gam[j] = gj;
         beta[j] = bj;
-#pragma unroll
-        for (int q = 0; q < ROWS; q++) {
-            const int i = q * G + glane;
-            if (i > j) A[q][j] *= scal;
-            else if (i == j) A[q][j] = bj;
-        }
+        inv_beta[j] = ib;
+        v0[j] = vj;
         double dot[NC];
 #pragma unroll
         for (int l = j + 1; l < NC; l++) {
@@ -150,7 +173,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) pl += A[q][l];
+                if (i == j) pl = fma(vj, A[q][l], pl);
                 else if (i > j) pl = fma(A[q][j], A[q][l], pl);
             }
             dot[l] = pl;
@@ -159,15 +182,18 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         for (int l = j + 1; l < NC; l++) dot[l] = group_sum<G>(dot[l]);
 #pragma unroll
         for (int l = j + 1; l < NC; l++) {
-            const double td = tj * dot[l];
+            const double td = gj * dot[l];
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) A[q][l] -= td;
+                if (i == j) A[q][l] = fma(-td, vj, A[q][l]);
                 else if (i > j) A[q][l] = fma(-td, A[q][j], A[q][l]);
             }
         }
-    }
+#pragma unroll
+        for (int q = 0; q < ROWS; q++)
+            if (q * G + glane == j) A[q][j] = bj;  // R_jj; v_j lives in v0[j]
+    });
 
     // ---- R (and Q^T b) to shared memory
 #pragma unroll
@@ -175,19 +201,12 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         const int i = q * G + glane;
         if (i < K) {
 #pragma unroll
-            for (int l = 1; l < K; l++)
-                if (l > i) sR[i * K + l] = A[q][l];
+            for (int l = 0; l < K; l++)
+                if (l >= i) sR[i * K + l] = A[q][l];
             if (SOLVE) sQ[i] = A[q][NC - 1];
         }
     }
-    if (glane == 0) {
-#pragma unroll
-        for (int j = 0; j < K; j++) sR[j * K + j] = beta[j];
-    }
     __syncwarp();
-    double inv_beta[K];
-#pragma unroll
-    for (int j = 0; j < K; j++) inv_beta[j] = 1.0 / beta[j];
 
     // ---- rank test: kappa_1(R) = ||R||_1 ||R^-1||_1 (lane l owns column l)
     double colsum = 0.0, invsum = 0.0;
@@ -210,8 +229,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     const bool singular = !ridge && !(kappa < kSingularKappa);
     const int status = empty ? FM_FIT_EMPTY : (singular ? FM_FIT_SINGULAR : FM_FIT_OK);
 
-    double mono_t[K];
-    eval_monos<DIM, DEG>(t, mono_t);
     if (SOLVE) {
         // c_scaled = R^-1 (Q^T b), coeffs = c_scaled / s^deg (_ext.pyx:411-412)
         double cs[K];
@@ -220,21 +237,36 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double acc = sQ[i];
 #pragma unroll
             for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], cs[c], acc);
-            cs[i] = acc / beta[i];
+            cs[i] = acc * inv_beta[i];
         }
-        double v = 0.0;
 #pragma unroll
-        for (int c = 0; c < K; c++) {
-            coeffs[c] = __ddiv_rn(cs[c], spow[c]);
-            v = add_rn(v, mul_rn(coeffs[c], mono_t[c]));
+        for (int c = 0; c < K; c++) coeffs[c] = __ddiv_rn(cs[c], spow[c]);
+        if (centering) {
+            value = coeffs[0];  // _ext.pyx:413-414
+        } else {
+            double mono_t[K];
+            eval_monos<DIM, DEG>(t, mono_t);
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < K; c++) v = add_rn(v, mul_rn(coeffs[c], mono_t[c]));
+            value = v;  // _ext.pyx:415-425
         }
-        value = fp.centering ? coeffs[0] : v;  // _ext.pyx:413-425
     } else {
         // z = R^-T g
+        double g[K];
+        if (centering) {
+#pragma unroll
+            for (int i = 0; i < K; i++) g[i] = i == 0 ? 1.0 : 0.0;
+        } else {
+            double mono_t[K];
+            eval_monos<DIM, DEG>(t, mono_t);
+#pragma unroll
+            for (int i = 0; i < K; i++) g[i] = __ddiv_rn(mono_t[i], spow[i]);
+        }
         double z[K];
 #pragma unroll
         for (int i = 0; i < K; i++) {
-            double acc = fp.centering ? (i == 0 ? 1.0 : 0.0) : __ddiv_rn(mono_t[i], spow[i]);
+            double acc = g[i];
 #pragma unroll
             for (int c = 0; c < i; c++) acc = fma(-sR[c * K + i], z[c], acc);
             z[i] = acc * inv_beta[i];
@@ -249,24 +281,25 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
                 if (i == c) v = z[c];
             yy[q] = v;
         }
-        // y = H_0 H_1 ... H_{K-1} [z; 0]
-#pragma unroll
-        for (int j = K - 1; j >= 0; j--) {
+        // y = H_0 H_1 ... H_{K-1} [z; 0]  (static_for: a runtime j would
+        // move A into local memory)
+        static_for<0, K>([&](auto jj) {
+            constexpr int j = K - 1 - decltype(jj)::value;
             double pl = 0.0;
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) pl += yy[q];
+                if (i == j) pl = fma(v0[j], yy[q], pl);
                 else if (i > j) pl = fma(A[q][j], yy[q], pl);
             }
-            const double td = tau[j] * group_sum<G>(pl);
+            const double td = gam[j] * group_sum<G>(pl);
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) yy[q] -= td;
+                if (i == j) yy[q] = fma(-td, v0[j], yy[q]);
                 else if (i > j) yy[q] = fma(-td, A[q][j], yy[q]);
             }
-        }
+        });
 #pragma unroll
         for (int q = 0; q < ROWS; q++) y[q] = valid[q] ? w[q] * yy[q] : 0.0;
     }

@@ -113,16 +113,30 @@ __global__ void k_bbox(const double *__restrict__ pts, int64_t n, unsigned long 
             mx[a] = fmax(mx[a], v);
         }
     }
+    // warp, then block reduction: one atomic pair per axis and block
+    __shared__ double s_mn[8][DIM], s_mx[8][DIM];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int a = 0; a < DIM; a++) {
         for (int o = 16; o > 0; o >>= 1) {
             mn[a] = fmin(mn[a], __shfl_xor_sync(FM_FULL_MASK, mn[a], o));
             mx[a] = fmax(mx[a], __shfl_xor_sync(FM_FULL_MASK, mx[a], o));
         }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&acc[a], dkey(mn[a]));
-            atomicMax(&acc[DIM + a], dkey(mx[a]));
+        if (lane == 0) {
+            s_mn[wid][a] = mn[a];
+            s_mx[wid][a] = mx[a];
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < DIM) {
+        const int a = threadIdx.x;
+        double lo = s_mn[0][a], hi = s_mx[0][a];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+            lo = fmin(lo, s_mn[w][a]);
+            hi = fmax(hi, s_mx[w][a]);
+        }
+        atomicMin(&acc[a], dkey(lo));
+        atomicMax(&acc[DIM + a], dkey(hi));
     }
 }
 

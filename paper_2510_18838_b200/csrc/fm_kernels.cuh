@@ -191,37 +191,64 @@ __global__ void __launch_bounds__(kBlock) k_support_fill(SearchArgs s, const int
     }
 }
 
-// --------------------------------------------------- fused fill + fit
-// OP: writes operator rows (col, val) at offsets[t].  SOLVE: writes
-// values[t] for the scalar field src_val (no support materialised).
-template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
-__global__ void __launch_bounds__(kBlock) k_fused_fit(SearchArgs s, const int64_t *__restrict__ offsets,
-                                                      int cap, int rbf_kind, double rbf_a, fm_fit fp,
-                                                      const double *__restrict__ src,
-                                                      const double *__restrict__ src_val,
-                                                      int32_t *__restrict__ col,
-                                                      double *__restrict__ val,
-                                                      double *__restrict__ values,
-                                                      uint8_t *__restrict__ status,
-                                                      int32_t *__restrict__ stats) {
+// ------------------------------------------------------- operator build
+// One launch builds the fits of positions k = klist[i] (or i) of the
+// processing order; target t = perm[k].  The support of each target comes
+// from the select pass's slot buffer (FROM_SLOTS: sorted ids + grid
+// positions, no search) or is re-gathered here (rescan: overflow targets,
+// and the standalone fm_build_operator / fm_transfer_values ABI).
+// OP: operator row written at offsets[k] (rows stored in processing order).
+// SOLVE: values[t] for the scalar field src_val.
+struct BuildArgs {
+    const int32_t *klist;  // positions to process, or null for 0..nk-1
+    int64_t nk;
+    const int32_t *slot_id;
+    const int32_t *slot_pos;
+    int slot_cap;
+    const int32_t *counts;  // support size per target (FROM_SLOTS)
+    const int64_t *offsets;
+    int cap;  // rescan list capacity
+    int rbf_kind;
+    double rbf_a;
+    fm_fit fp;
+    const double *src_val;
+    int32_t *col;
+    double *val;
+    double *values;
+    uint8_t *status;
+    int32_t *stats;
+};
+
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
+__global__ void __launch_bounds__(kBlock) k_build(SearchArgs s, BuildArgs b) {
     constexpr int K = Monos<DIM, DEG>::K;
     extern __shared__ __align__(16) char smem[];
     int nfail = 0, first_fail = INT32_MAX;
-    GroupSmem<G> gs = carve<G>(smem, cap, K);
+    GroupSmem<G> gs = carve<G>(smem, FROM_SLOTS ? 0 : b.cap, K);
     constexpr int GPW = 32 / G;
     const int lane = threadIdx.x & 31, glane = lane & (G - 1);
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    for (int64_t tile = warp; tile * GPW < s.nt; tile += nwarps) {
-        const int64_t k = tile * GPW + lane / G;
-        const bool active = k < s.nt;
+    for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
+        const int64_t ii = tile * GPW + lane / G;
+        bool active = ii < b.nk;
+        const int64_t k = active ? (b.klist ? (int64_t)b.klist[ii] : ii) : 0;
         const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
         double t[DIM];
         load_target<DIM>(s.targets, tid, active, t);
         const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
-        int m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r, active,
-                                       lane, glane, *gs.rt, gs.id, gs.pos, gs.sid, gs.spos, cap);
-        if (m > cap) m = cap;  // host sizes cap >= max count
+        int m;
+        if (FROM_SLOTS) {
+            m = active ? b.counts[tid] : 0;
+            if (m > b.slot_cap) {  // overflow: built by the rescan launch
+                active = false;
+                m = 0;
+            }
+        } else {
+            m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r, active,
+                                       lane, glane, *gs.rt, gs.id, gs.pos, gs.sid, gs.spos, b.cap);
+            if (m > b.cap) m = b.cap;  // host sizes cap >= max count
+        }
         bool valid[ROWS];
         double p[ROWS][DIM], w[ROWS], f[ROWS];
         int32_t ids[ROWS];
@@ -235,42 +262,145 @@ __global__ void __launch_bounds__(kBlock) k_fused_fit(SearchArgs s, const int64_
 #pragma unroll
             for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
             if (valid[q]) {
-                ids[q] = gs.sid[i];
-                load_point<DIM>(s.sorted_pts, gs.spos[i], p[q]);
+                int32_t pos;
+                if (FROM_SLOTS) {
+                    ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
+                    pos = __ldg(b.slot_pos + k * b.slot_cap + i);
+                } else {
+                    ids[q] = gs.sid[i];
+                    pos = gs.spos[i];
+                }
+                load_point<DIM>(s.sorted_pts, pos, p[q]);
                 const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
-                w[q] = fabs(rbf_one(rbf_kind, rbf_a, r, d));  // pointwise.py:301
-                if (SOLVE) f[q] = __ldg(src_val + ids[q]);
+                w[q] = fabs(rbf_one(b.rbf_kind, b.rbf_a, r, d));  // pointwise.py:301
+                if (SOLVE) f[q] = __ldg(b.src_val + ids[q]);
             }
         }
         double y[ROWS], coeffs[K], value = 0.0;
-        const int st = fit_rows<DIM, DEG, G, ROWS, SOLVE>(fp, t, m, valid, p, w, f, lane, glane,
+        const int st = fit_rows<DIM, DEG, G, ROWS, SOLVE>(b.fp, t, m, valid, p, w, f, lane, glane,
                                                           gs.sR, gs.sQ, y, coeffs, value);
         if (active) {
             if (glane == 0) {
-                status[tid] = (uint8_t)st;
+                b.status[tid] = (uint8_t)st;
                 if (st != FM_FIT_OK) {
                     nfail++;
                     first_fail = min(first_fail, (int)tid);
                 }
             }
             if (SOLVE) {
-                if (glane == 0) values[tid] = st == FM_FIT_OK ? value : NAN;
+                if (glane == 0) b.values[tid] = st == FM_FIT_OK ? value : NAN;
             } else {
-                const int64_t off = offsets[tid];
+                const int64_t off = b.offsets[k];
 #pragma unroll
                 for (int q = 0; q < ROWS; q++) {
                     if (valid[q]) {
                         const int i = q * G + glane;
-                        col[off + i] = ids[q];
-                        val[off + i] = st == FM_FIT_OK ? y[q] : NAN;
+                        b.col[off + i] = ids[q];
+                        b.val[off + i] = st == FM_FIT_OK ? y[q] : NAN;
                     }
                 }
             }
         }
         __syncwarp();
     }
-    if (stats) warp_flush_pair(stats, nfail, first_fail);
-    (void)src;
+    if (b.stats) warp_flush_pair(b.stats, nfail, first_fail);
+}
+
+// ----------------------------------------------------- select pass
+// Count pass that also emits each target's support, sorted by source id,
+// into a fixed-stride slot buffer indexed by processing position
+// (slot_id/slot_pos[k*slot_cap + i]).  Targets whose support exceeds the
+// slot (or the per-group list) are appended to overflow (positions k) and
+// rebuilt by the rescan build.
+// stats[8]: max, min, #short, first short, #status, first status, #overflow, 0.
+template <int DIM, int G>
+__global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_required, int lcap,
+                                                   int32_t *__restrict__ counts,
+                                                   double *__restrict__ radii,
+                                                   uint8_t *__restrict__ status,
+                                                   int32_t *__restrict__ slot_id,
+                                                   int32_t *__restrict__ slot_pos, int slot_cap,
+                                                   int32_t *__restrict__ overflow,
+                                                   int32_t *__restrict__ stats) {
+    extern __shared__ __align__(16) char smem[];
+    constexpr int GPW = 32 / G;
+    const int grp = threadIdx.x / G;
+    const size_t per = ((size_t)lcap * 16 + sizeof(RowTable<G>) + 15) & ~(size_t)15;
+    char *base = smem + grp * per;
+    ListBuf lb;
+    lb.d = reinterpret_cast<double *>(base);
+    lb.id = reinterpret_cast<int32_t *>(base + (size_t)lcap * 8);
+    lb.pos = lb.id + lcap;
+    lb.cap = lcap;
+    RowTable<G> &rt = *reinterpret_cast<RowTable<G> *>(base + (size_t)lcap * 16);
+    const int lane = threadIdx.x & 31, glane = lane & (G - 1);
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    int local_max = 0, local_min = INT32_MAX;
+    int nshort = 0, first_short = INT32_MAX, nstat = 0, first_stat = INT32_MAX;
+    for (int64_t tile = warp; tile * GPW < s.nt; tile += nwarps) {
+        const int64_t k = tile * GPW + lane / G;
+        const bool active = k < s.nt;
+        const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+        double t[DIM];
+        load_target<DIM>(s.targets, tid, active, t);
+        double r;
+        uint8_t st;
+        bool listed;
+        const int m = select_target<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, s.sel,
+                                            active, lane, glane, rt, lb, r, st, listed);
+        if (active) {
+            if (listed && m <= slot_cap) {
+                // rank sort by id straight into the slot (ids are distinct)
+                int32_t *oid = slot_id + k * slot_cap;
+                int32_t *opos = slot_pos + k * slot_cap;
+                for (int e = glane; e < m; e += G) {
+                    const int32_t id = lb.id[e];
+                    int rank = 0;
+                    for (int f2 = 0; f2 < m; f2++) rank += lb.id[f2] < id;
+                    oid[rank] = id;
+                    opos[rank] = lb.pos[e];
+                }
+            } else if (glane == 0) {
+                overflow[atomicAdd(stats + 6, 1)] = (int32_t)k;
+            }
+            if (glane == 0) {
+                counts[tid] = m;
+                if (s.sel.adaptive) {
+                    if (radii) radii[tid] = r;
+                    if (status) status[tid] = st;
+                    if (st) {
+                        nstat++;
+                        first_stat = min(first_stat, (int)tid);
+                    }
+                }
+                local_max = max(local_max, m);
+                local_min = min(local_min, m);
+                if (m < min_required) {
+                    nshort++;
+                    first_short = min(first_short, (int)tid);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    local_max = __reduce_max_sync(FM_FULL_MASK, local_max);
+    local_min = __reduce_min_sync(FM_FULL_MASK, (unsigned)local_min);
+    if (lane == 0) {
+        atomicMax(stats + 0, local_max);
+        atomicMin(stats + 1, local_min);
+    }
+    warp_flush_pair(stats + 2, nshort, first_short);
+    warp_flush_pair(stats + 4, nstat, first_stat);
+}
+
+// counts in processing order (input of the ordered offsets scan)
+static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
+                                const int32_t *__restrict__ perm, int64_t n,
+                                int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = counts[perm ? perm[i] : i];
 }
 
 // ------------------------------------------------- fit_many (CSR input)
@@ -378,20 +508,25 @@ int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *i
     return FM_OK;
 }
 
-template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
-int launch_fused_rows(const SearchArgs &s, const int64_t *offsets, int cap, const fm_rbf &rbf,
-                      const fm_fit &fp, const double *src, const double *src_val, int32_t *col,
-                      double *val, double *values, uint8_t *status, int32_t *stats,
-                      cudaStream_t st) {
-    constexpr int K = Monos<DIM, DEG>::K;
-    const size_t sm = block_smem_bytes<G>(cap, K);
+constexpr int kSelectListCap = 128;  // per-group candidate list of the select pass
+
+template <int DIM>
+int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,
+                  uint8_t *status, int32_t *slot_id, int32_t *slot_pos, int slot_cap,
+                  int32_t *overflow, int32_t *stats, cudaStream_t st) {
+    constexpr int G = 16;
+    k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0);
+    if (s.nt == 0) return FM_OK;
+    const int lcap = slot_cap > kSelectListCap ? slot_cap : kSelectListCap;
+    const size_t per = ((size_t)lcap * 16 + sizeof(RowTable<G>) + 15) & ~(size_t)15;
+    const size_t sm = per * (kBlock / G);
     if (sm > 200 * 1024) return FM_ERR_UNSUPPORTED;
-    auto kern = k_fused_fit<DIM, DEG, G, ROWS, SOLVE>;
     if (sm > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<grid_blocks(s.nt, kBlock / G, 16), kBlock, sm, st>>>(s, offsets, cap, rbf.kind, rbf.a, fp,
-                                                               src, src_val, col, val, values,
-                                                               status, stats);
+        cudaFuncSetAttribute(k_select<DIM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+    k_select<DIM, G><<<grid_blocks(s.nt, kBlock / G, 16), kBlock, sm, st>>>(
+        s, min_required, lcap, counts, radii, status, slot_id, slot_pos, slot_cap, overflow,
+        stats);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -402,25 +537,36 @@ inline int fit_rows_needed(int max_m, int K, double lam) {
     return r < K ? K : r;
 }
 
-template <int DIM, int DEG, bool SOLVE>
-int launch_fused(const SearchArgs &s, const int64_t *offsets, int cap, const fm_rbf &rbf,
-                 const fm_fit &fp, const double *src, const double *src_val, int32_t *col,
-                 double *val, double *values, uint8_t *status, int32_t *stats, cudaStream_t st) {
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
+int launch_build_rows(const SearchArgs &s, const BuildArgs &b, cudaStream_t st) {
     constexpr int K = Monos<DIM, DEG>::K;
-    constexpr int G = FitShape<DIM, DEG>::G;
-    if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 2, 1);
-    if (s.nt == 0) return FM_OK;
-    if (cap < 1) cap = 1;
-    const int need = fit_rows_needed(cap, K, fp.lam);
-#define FM_FUSED(R) \
-    launch_fused_rows<DIM, DEG, G, R, SOLVE>(s, offsets, cap, rbf, fp, src, src_val, col, val, values, status, stats, st)
-    if (need <= G) return FM_FUSED(1);
-    if (need <= 2 * G) return FM_FUSED(2);
-    if (need <= 4 * G) return FM_FUSED(4);
-    if constexpr (G == 16) {
-        if (need <= 8 * G) return FM_FUSED(8);
+    const size_t sm = block_smem_bytes<G>(FROM_SLOTS ? 0 : b.cap, K);
+    if (sm > 200 * 1024) return FM_ERR_UNSUPPORTED;
+    auto kern = k_build<DIM, DEG, G, ROWS, SOLVE, FROM_SLOTS>;
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid_blocks(b.nk, kBlock / G, 16), kBlock, sm, st>>>(s, b);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+// (G lanes, ROWS rows per lane) with G*ROWS >= rows needed: groups of
+// FitShape::G lanes (8/16/32 by k) while ROWS <= 4, 32-lane groups beyond.
+template <int DIM, int DEG, bool SOLVE, bool FROM_SLOTS>
+int launch_build(const SearchArgs &s, const BuildArgs &b, int max_m, cudaStream_t st) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    constexpr int G0 = FitShape<DIM, DEG>::G;
+    if (b.nk == 0) return FM_OK;
+    const int need = fit_rows_needed(max_m, K, b.fp.lam);
+#define FM_BUILD(GG, R) launch_build_rows<DIM, DEG, GG, R, SOLVE, FROM_SLOTS>(s, b, st)
+    if (need <= G0) return FM_BUILD(G0, 1);
+    if (need <= 2 * G0) return FM_BUILD(G0, 2);
+    if (need <= 4 * G0) return FM_BUILD(G0, 4);
+    if constexpr (G0 < 32) {
+        if (need <= 128) return FM_BUILD(32, 4);
     }
-#undef FM_FUSED
+    if (need <= 256) return FM_BUILD(32, 8);
+#undef FM_BUILD
     return FM_ERR_UNSUPPORTED;
 }
 
@@ -430,25 +576,25 @@ int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const i
                     const double *src_val, double *values, double *coeffs, uint8_t *status,
                     int32_t *stats, cudaStream_t st) {
     constexpr int K = Monos<DIM, DEG>::K;
-    constexpr int G = FitShape<DIM, DEG>::G;
+    constexpr int G0 = FitShape<DIM, DEG>::G;
     if (stats) k_stats_init<<<1, 32, 0, st>>>(stats, 2, 1);
     if (nt == 0) return FM_OK;
     const int need = fit_rows_needed(max_m, K, fp.lam);
-    const int blocks = grid_blocks(nt, kBlock / G, 16);
-#define FM_FITMANY(R)                                                                       \
-    do {                                                                                    \
-        k_fit_many<DIM, DEG, G, R><<<blocks, kBlock, 0, st>>>(fp, targets, nt, sup_off, sup_idx, \
-                                                              sup_w, src, src_val, values,  \
-                                                              coeffs, status, stats);       \
-        FM_CHECK_LAUNCH();                                                                  \
-        return FM_OK;                                                                       \
+#define FM_FITMANY(GG, R)                                                                    \
+    do {                                                                                     \
+        k_fit_many<DIM, DEG, GG, R><<<grid_blocks(nt, kBlock / GG, 16), kBlock, 0, st>>>(    \
+            fp, targets, nt, sup_off, sup_idx, sup_w, src, src_val, values, coeffs, status,  \
+            stats);                                                                          \
+        FM_CHECK_LAUNCH();                                                                   \
+        return FM_OK;                                                                        \
     } while (0)
-    if (need <= G) FM_FITMANY(1);
-    if (need <= 2 * G) FM_FITMANY(2);
-    if (need <= 4 * G) FM_FITMANY(4);
-    if constexpr (G == 16) {
-        if (need <= 8 * G) FM_FITMANY(8);
+    if (need <= G0) FM_FITMANY(G0, 1);
+    if (need <= 2 * G0) FM_FITMANY(G0, 2);
+    if (need <= 4 * G0) FM_FITMANY(G0, 4);
+    if constexpr (G0 < 32) {
+        if (need <= 128) FM_FITMANY(32, 4);
     }
+    if (need <= 256) FM_FITMANY(32, 8);
 #undef FM_FITMANY
     return FM_ERR_UNSUPPORTED;
 }
@@ -461,11 +607,12 @@ int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const i
     int dim##N##_count(const SearchArgs &, int32_t, int32_t *, double *, uint8_t *, int32_t *,   \
                        cudaStream_t);                                                             \
     int dim##N##_fill(const SearchArgs &, const int64_t *, int, int64_t *, double *, int,        \
-                      double, double *, cudaStream_t);
+                      double, double *, cudaStream_t);                                            \
+    int dim##N##_select(const SearchArgs &, int32_t, int32_t *, double *, uint8_t *, int32_t *,  \
+                        int32_t *, int, int32_t *, int32_t *, cudaStream_t);
 #define FM_DECLARE_DEG(N, P)                                                                      \
-    int dim##N##_deg##P##_fused(bool, const SearchArgs &, const int64_t *, int, const fm_rbf &,  \
-                                const fm_fit &, const double *, const double *, int32_t *,       \
-                                double *, double *, uint8_t *, int32_t *, cudaStream_t);          \
+    int dim##N##_deg##P##_build(bool, bool, const SearchArgs &, const BuildArgs &, int,          \
+                                cudaStream_t);                                                    \
     int dim##N##_deg##P##_fit_many(const fm_fit &, const double *, int64_t, const int64_t *,     \
                                    const int64_t *, const double *, int, const double *,         \
                                    const double *, double *, double *, uint8_t *, int32_t *,     \
@@ -489,17 +636,21 @@ FM_DECLARE_DEG(5, 0) FM_DECLARE_DEG(5, 1) FM_DECLARE_DEG(5, 2)
     int dim##N##_fill(const SearchArgs &s, const int64_t *o, int cap, int64_t *idx, double *d,    \
                       int kind, double a, double *w, cudaStream_t stream) {                        \
         return launch_fill<N>(s, o, cap, idx, d, kind, a, w, stream);                              \
+    }                                                                                              \
+    int dim##N##_select(const SearchArgs &s, int32_t need, int32_t *c, double *r, uint8_t *st,    \
+                        int32_t *sid, int32_t *spos, int scap, int32_t *ovf, int32_t *stats,       \
+                        cudaStream_t stream) {                                                     \
+        return launch_select<N>(s, need, c, r, st, sid, spos, scap, ovf, stats, stream);           \
     }
 
 #define FM_DEFINE_DEG(N, P)                                                                        \
-    int dim##N##_deg##P##_fused(bool solve, const SearchArgs &s, const int64_t *o, int cap,       \
-                                const fm_rbf &rbf, const fm_fit &fp, const double *src,            \
-                                const double *sv, int32_t *col, double *val, double *vals,         \
-                                uint8_t *st, int32_t *stats, cudaStream_t stream) {                \
-        return solve ? launch_fused<N, P, true>(s, o, cap, rbf, fp, src, sv, col, val, vals, st,   \
-                                                stats, stream)                                     \
-                     : launch_fused<N, P, false>(s, o, cap, rbf, fp, src, sv, col, val, vals, st,  \
-                                                 stats, stream);                                   \
+    int dim##N##_deg##P##_build(bool solve, bool slots, const SearchArgs &s, const BuildArgs &b,  \
+                                int max_m, cudaStream_t stream) {                                  \
+        if (slots)                                                                                 \
+            return solve ? launch_build<N, P, true, true>(s, b, max_m, stream)                     \
+                         : launch_build<N, P, false, true>(s, b, max_m, stream);                   \
+        return solve ? launch_build<N, P, true, false>(s, b, max_m, stream)                        \
+                     : launch_build<N, P, false, false>(s, b, max_m, stream);                      \
     }                                                                                              \
     int dim##N##_deg##P##_fit_many(const fm_fit &fp, const double *t, int64_t nt,                 \
                                    const int64_t *so, const int64_t *si, const double *sw, int mm, \

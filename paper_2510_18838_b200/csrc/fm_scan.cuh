@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const TIn *__restr
 }
 
 // exclusive scan of the block sums in place (one block, chunked)
-__global__ void __launch_bounds__(1024) k_scan_sums(long long *__restrict__ sums, int64_t nb) {
+static __global__ void __launch_bounds__(1024) k_scan_sums(long long *__restrict__ sums, int64_t nb) {
     __shared__ long long warp_tot[32];
     __shared__ long long carry_s;
     if (threadIdx.x == 0) carry_s = 0;

@@ -29,33 +29,45 @@ struct RowTable {
     int32_t pref[G];
 };
 
-// Enumerate the candidates of the window of (t, r) for the calling group.
-// Every lane of the WARP must call this (collectives inside); `active` false
-// makes the group's window empty.  `visit(pos, valid)` is called the same
-// (warp-uniform) number of times on every lane; pos is an index into the
-// cell-sorted arrays when valid.
-template <int DIM, int G, class Visit>
-__device__ __forceinline__ void for_each_candidate(const GridDev &g,
-                                                   const int32_t *__restrict__ cell_start,
-                                                   const double *t, double r, bool active,
-                                                   int glane, RowTable<G> &rt, Visit &&visit) {
-    const double rs = r * (1.0 + kSlackRel);
+// Window of (t, r) for the calling group, enumerated as row chunks of up to
+// G rows each, flattened to candidate indices with a group prefix sum.
+//   Window<DIM,G> w(g, t, r, active);
+//   for (int ch = 0; ch < w.nchunks_w; ch++) {
+//       const int iters = w.chunk(g, cell_start, t, ch, glane, rt);
+//       for (int it = 0; it < iters; it++) { bool v; int pos = w.pos(it, glane, rt, v); ... }
+//       __syncwarp();
+//   }
+// Every lane of the WARP must run the loops (collectives inside; the trip
+// counts are warp-uniform); `active` false makes the group's window empty.
+template <int DIM, int G>
+struct Window {
     int64_t clo[kMaxDim], chi[kMaxDim], stride[kMaxDim];
-    int64_t nrows = active ? 1 : 0;
-    int64_t st = 1;
+    int64_t nrows;
+    int nchunks_w;
+    double rs2, eps_r2;
+    int total, cursor;
+
+    __device__ __forceinline__ Window(const GridDev &g, const double *t, double r, bool active) {
+        const double rs = r * (1.0 + kSlackRel);
+        nrows = active ? 1 : 0;
+        int64_t st = 1;
 #pragma unroll
-    for (int a = 0; a < DIM; a++) {
-        clo[a] = cell_of(t[a] - rs, g.lo[a], g.inv_d[a], g.n[a]);
-        chi[a] = cell_of(t[a] + rs, g.lo[a], g.inv_d[a], g.n[a]);
-        stride[a] = st;
-        st *= g.n[a];
-        if (a > 0) nrows *= (chi[a] - clo[a] + 1);
+        for (int a = 0; a < DIM; a++) {
+            clo[a] = cell_of(t[a] - rs, g.lo[a], g.inv_d[a], g.n[a]);
+            chi[a] = cell_of(t[a] + rs, g.lo[a], g.inv_d[a], g.n[a]);
+            stride[a] = st;
+            st *= g.n[a];
+            if (a > 0) nrows *= (chi[a] - clo[a] + 1);
+        }
+        nchunks_w = warp_max_int((int)((nrows + G - 1) / G));
+        rs2 = rs * rs;
+        eps_r2 = 8.0 * 2.220446049250313e-16 * rs2;
     }
-    const int nchunks = (int)((nrows + G - 1) / G);
-    const int nchunks_w = warp_max_int(nchunks);
-    const double rs2 = rs * rs;
-    const double eps_r2 = 8.0 * 2.220446049250313e-16 * rs2;
-    for (int ch = 0; ch < nchunks_w; ch++) {
+
+    // Row table of chunk ch (rows ch*G .. ch*G+G-1); returns the warp-uniform
+    // number of candidate iterations.
+    __device__ __forceinline__ int chunk(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                         const double *t, int ch, int glane, RowTable<G> &rt) {
         const int64_t row = (int64_t)ch * G + glane;
         int32_t start = 0, len = 0;
         if (row < nrows) {
@@ -89,20 +101,36 @@ __device__ __forceinline__ void for_each_candidate(const GridDev &g,
             }
         }
         const int incl = group_scan_incl<G>(len, glane);
-        const int total = __shfl_sync(FM_FULL_MASK, incl, (threadIdx.x & 31 & ~(G - 1)) + G - 1);
+        total = __shfl_sync(FM_FULL_MASK, incl, (threadIdx.x & 31 & ~(G - 1)) + G - 1);
         rt.start[glane] = start;
         rt.pref[glane] = incl - len;
         __syncwarp();
-        const int iters = warp_max_int((total + G - 1) / G);
-        int cursor = 0;
+        cursor = 0;
+        return warp_max_int((total + G - 1) / G);
+    }
+
+    // Candidate of iteration it for this lane (index into the cell-sorted arrays).
+    __device__ __forceinline__ int pos(int it, int glane, const RowTable<G> &rt, bool &valid) {
+        const int c = it * G + glane;
+        valid = c < total;
+        if (!valid) return 0;
+        while (cursor + 1 < G && c >= rt.pref[cursor + 1]) cursor++;
+        return rt.start[cursor] + (c - rt.pref[cursor]);
+    }
+};
+
+// Lambda form of the enumeration for the less hot paths.
+template <int DIM, int G, class Visit>
+__device__ __forceinline__ void for_each_candidate(const GridDev &g,
+                                                   const int32_t *__restrict__ cell_start,
+                                                   const double *t, double r, bool active,
+                                                   int glane, RowTable<G> &rt, Visit &&visit) {
+    Window<DIM, G> w(g, t, r, active);
+    for (int ch = 0; ch < w.nchunks_w; ch++) {
+        const int iters = w.chunk(g, cell_start, t, ch, glane, rt);
         for (int it = 0; it < iters; it++) {
-            const int c = it * G + glane;
-            const bool valid = c < total;
-            int pos = 0;
-            if (valid) {
-                while (cursor + 1 < G && c >= rt.pref[cursor + 1]) cursor++;
-                pos = rt.start[cursor] + (c - rt.pref[cursor]);
-            }
+            bool valid;
+            const int pos = w.pos(it, glane, rt, valid);
             visit(pos, valid);
         }
         __syncwarp();
@@ -211,6 +239,287 @@ __device__ __forceinline__ int collect_sorted(const GridDev &g, const int32_t *_
         s_spos[rank] = s_pos[e];
     }
     __syncwarp();
+    return m;
+}
+
+// ======================================================================
+// Selection with support lists (count pass that also emits the supports)
+// ======================================================================
+constexpr int kMaxGuess = 8;  // radii evaluated by the first multi-radius scan: r_0..r_8
+
+// Per-group list buffer in shared memory (discovery order): source id,
+// sorted position and distance of each kept candidate.
+struct ListBuf {
+    int32_t *id;
+    int32_t *pos;
+    double *d;
+    int cap;
+};
+
+// One window scan at radius radii[nr-1] that counts #{d < radii[j]} for all
+// j < nr at once (the reference's count at each radius of its growth
+// sequence, _ext.pyx:258-271) and appends every candidate with
+// d < radii[nr-1] to the group's list (entries beyond cap are counted, not
+// stored).  Warp-collective.
+// Smallest double T with fl(sqrt(T)) >= r (r > 0).  fl o sqrt is monotone,
+// so the reference's test fl(sqrt(d2)) < r (_ext.pyx:194-195) is exactly
+// d2 < T: the scans compare squared distances and never take a square root.
+__device__ __forceinline__ double sqrt_threshold(double r) {
+    double x = mul_rn(r, r);
+    if (!(x < INFINITY) || !(x > 0.0)) return x;
+    for (int it = 0; it < 64; it++) {  // step down while the predecessor still fails
+        const double xp = __longlong_as_double(__double_as_longlong(x) - 1);
+        if (xp > 0.0 && __dsqrt_rn(xp) >= r) x = xp;
+        else break;
+    }
+    for (int it = 0; it < 64; it++) {  // step up while x still passes
+        if (__dsqrt_rn(x) < r) x = __longlong_as_double(__double_as_longlong(x) + 1);
+        else break;
+    }
+    return x;
+}
+
+template <int DIM, int G, int NR>
+__device__ __forceinline__ void scan_counts(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                            const double *__restrict__ sorted_pts,
+                                            const int32_t *__restrict__ sorted_ids, const double *t,
+                                            const double (&radii)[NR], int nr, bool active,
+                                            int lane, int glane, RowTable<G> &rt, int (&cnt)[NR],
+                                            ListBuf &lb, int &nlist) {
+    double rscan = 0.0;  // radii[nr - 1], selected statically (keeps radii in registers)
+#pragma unroll
+    for (int j = 0; j < NR; j++)
+        if (active && j == nr - 1) rscan = radii[j];
+    // thresholds of radii[0..nr-1]: one lane each, then broadcast to the group
+    static_assert(NR <= G, "one lane per radius");
+    double my_r = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; j++)
+        if (glane == j) my_r = radii[j];
+    const double my_thr = (active && glane < nr) ? sqrt_threshold(my_r) : 0.0;
+    const int gbase = lane & ~(G - 1);
+    double thr[NR];
+    double thr_scan = 0.0;
+    static_for<0, NR>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        thr[j] = __shfl_sync(FM_FULL_MASK, my_thr, gbase + j);
+        if (j == nr - 1) thr_scan = thr[j];
+    });
+    const unsigned lt_mask = (1u << glane) - 1u;
+    Window<DIM, G> w(g, t, rscan, active);
+    for (int ch = 0; ch < w.nchunks_w; ch++) {
+        const int iters = w.chunk(g, cell_start, t, ch, glane, rt);
+        for (int it = 0; it < iters; it++) {
+            bool valid;
+            const int pos = w.pos(it, glane, rt, valid);
+            double d2 = INFINITY;
+            int32_t id = 0;
+            if (valid) {
+                double p[DIM];
+                id = __ldg(sorted_ids + pos);  // issued with the point load
+                load_point<DIM>(sorted_pts, pos, p);
+                d2 = dist2_rn<DIM>(p, t);
+            }
+            const bool keep = d2 < thr_scan;
+            const unsigned bits = group_bits<G>(__ballot_sync(FM_FULL_MASK, keep), lane);
+            if (keep) {
+                const int o = nlist + __popc(bits & lt_mask);
+                if (o < lb.cap) {
+                    lb.id[o] = id;
+                    lb.pos[o] = pos;
+                    lb.d[o] = d2;
+                }
+            }
+            nlist += __popc(bits);
+            static_for<0, NR>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                cnt[j] += __popc(group_bits<G>(__ballot_sync(FM_FULL_MASK, j < nr && d2 < thr[j]),
+                                               lane));
+            });
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+}
+
+// Density guess of the number of growth steps (2-D): sources in the 3x3
+// cell block around the target -> radius holding min_pts at that density.
+// Only a starting point: the result is exact whatever the guess.
+template <int DIM, int G>
+__device__ __forceinline__ int guess_steps(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                           const double *t, const fm_select &sel, bool active,
+                                           int glane) {
+    if (DIM != 2) return 0;
+    const int64_t nx = g.n[0], ny = g.n[1];
+    const int64_t cx = cell_of(t[0], g.lo[0], g.inv_d[0], nx);
+    const int64_t cy = cell_of(t[1], g.lo[1], g.inv_d[1], ny);
+    const int64_t x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < nx ? cx + 1 : nx - 1;
+    const int64_t y0 = cy > 0 ? cy - 1 : 0, y1 = cy + 1 < ny ? cy + 1 : ny - 1;
+    int n = 0;
+    if (active && glane <= y1 - y0) {
+        const int64_t row = (y0 + glane) * nx;
+        n = cell_start[row + x1 + 1] - cell_start[row + x0];
+    }
+    n = group_sum_int<G>(n);
+    if (!active) return 0;
+    const double area = (double)((x1 - x0 + 1) * (y1 - y0 + 1)) * g.d[0] * g.d[1];
+    // smallest k with r0 * growth^k >= r_est, r_est^2 = min_pts / (pi rho)
+    const float r2_est = (float)((double)sel.min_pts * area /
+                                 (3.14159265f * (n > 0 ? (float)n : 0.5f)));
+    float r = (float)sel.r0, g2 = (float)sel.growth;
+    int k = 0;
+    while (k < kMaxGuess && r * r < r2_est) {
+        r *= g2;
+        k++;
+    }
+    return k;
+}
+
+// Final support of one target for fixed or adaptive selection, exactly the
+// reference's (fixed: d < r_c; adaptive: the first radius of the sequence
+// r0, min(r*growth, r_max), ... holding >= min_pts sources, status 1 when
+// r_max is reached short).  Returns the count m; when `listed` is true the
+// group's buffer holds all m supports (discovery order), otherwise m > cap.
+// Warp-collective.
+template <int DIM, int G>
+__device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                             const double *__restrict__ sorted_pts,
+                                             const int32_t *__restrict__ sorted_ids,
+                                             const double *t, const fm_select &sel, bool active,
+                                             int lane, int glane, RowTable<G> &rt, ListBuf &lb,
+                                             double &r_out, uint8_t &status, bool &listed) {
+    constexpr int NR = kMaxGuess + 1;
+    double radii[NR];
+    int nr = 1;
+    if (sel.adaptive) {
+        const int kg = guess_steps<DIM, G>(g, cell_start, t, sel, active, glane);
+        double r = sel.r0;
+        bool stop = false;
+#pragma unroll
+        for (int j = 0; j < NR; j++) {
+            radii[j] = r;
+            if (!stop && j <= kg) {
+                nr = j + 1;
+                if (r >= sel.r_max) {
+                    stop = true;
+                } else {
+                    r = r * sel.growth;
+                    if (r > sel.r_max) r = sel.r_max;
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NR; j++) radii[j] = sel.r_c;
+    }
+    int cnt[NR];
+#pragma unroll
+    for (int j = 0; j < NR; j++) cnt[j] = 0;
+    int nlist = 0;
+    scan_counts<DIM, G, NR>(g, cell_start, sorted_pts, sorted_ids, t, radii, nr, active, lane,
+                            glane, rt, cnt, lb, nlist);
+    // first radius of the scanned prefix of the sequence that holds min_pts
+    int m = 0;
+    double rf = 0.0, rlast = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; j++)
+        if (j == nr - 1) {
+            m = cnt[j];
+            rf = radii[j];
+        }
+    rlast = rf;
+    status = 0;
+    bool done = !active;
+    if (active) {
+        if (!sel.adaptive) {
+            done = true;
+        } else {
+            int jf = -1;
+#pragma unroll
+            for (int j = 0; j < NR; j++)
+                if (jf < 0 && j < nr && cnt[j] >= sel.min_pts) jf = j;
+#pragma unroll
+            for (int j = 0; j < NR; j++)
+                if (j == jf) {
+                    m = cnt[j];
+                    rf = radii[j];
+                }
+            if (jf >= 0) {
+                done = true;
+            } else if (rf >= sel.r_max) {
+                status = 1;
+                done = true;
+            }
+        }
+    }
+    // continue the sequence one radius at a time (_ext.pyx:259-270)
+    bool fresh = false;  // list rebuilt at exactly rf
+    while (__any_sync(FM_FULL_MASK, !done)) {
+        double r1[1] = {0.0};
+        int c1[1] = {0};
+        const bool go = !done;
+        if (go) {
+            rf = rf * sel.growth;
+            if (rf > sel.r_max) rf = sel.r_max;
+            r1[0] = rf;
+            nlist = 0;
+        }
+        int nl = nlist;
+        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, go, lane, glane,
+                               rt, c1, lb, nl);
+        if (go) {
+            nlist = nl;
+            m = c1[0];
+            fresh = true;
+            if (m >= sel.min_pts) {
+                done = true;
+            } else if (rf >= sel.r_max) {
+                status = 1;
+                done = true;
+            }
+        }
+    }
+    // keep only d < rf when the list came from a wider scan; rescan when the
+    // wider scan overflowed the buffer but the final support fits
+    const bool wide = active && !fresh && rf < rlast;
+    const bool rescan = wide && nlist > lb.cap && m <= lb.cap;
+    if (__any_sync(FM_FULL_MASK, rescan)) {
+        double r1[1] = {rescan ? rf : 0.0};
+        int c1[1] = {0};
+        int nl = 0;
+        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, rescan, lane,
+                               glane, rt, c1, lb, nl);
+        if (rescan) nlist = nl;
+    }
+    const bool filter = wide && !rescan && nlist <= lb.cap;
+    const int nf = filter ? nlist : 0;
+    const int iters = warp_max_int((nf + G - 1) / G);
+    const double thr_f = filter ? sqrt_threshold(rf) : 0.0;
+    int kept = 0;
+    const unsigned lt_mask = (1u << glane) - 1u;
+    for (int it = 0; it < iters; it++) {
+        const int e = it * G + glane;
+        int32_t id = 0, pos = 0;
+        double d = 0.0;  // squared distance
+        const bool in = e < nf;
+        if (in) {
+            id = lb.id[e];
+            pos = lb.pos[e];
+            d = lb.d[e];
+        }
+        const bool keep = in && d < thr_f;
+        const unsigned bits = group_bits<G>(__ballot_sync(FM_FULL_MASK, keep), lane);
+        if (keep) {
+            const int o = kept + __popc(bits & lt_mask);
+            lb.id[o] = id;
+            lb.pos[o] = pos;
+            lb.d[o] = d;
+        }
+        kept += __popc(bits);
+    }
+    __syncwarp();
+    r_out = rf;
+    listed = active && m <= lb.cap;
     return m;
 }
 

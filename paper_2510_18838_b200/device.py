@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import FmFit, FmGrid, FmRbf, FmSelect, check, ptr
+from ._lib import FmFit, FmGrid, FmLists, FmRbf, FmSelect, check, ptr
 from .locate import grid_geometry
 
 INT32_MAX = 2 ** 31 - 1
@@ -77,6 +77,7 @@ class SourceCloud:
                 else:
                     bbox = device_bbox(self.pts)
             geom = grid_geometry(bbox[0], bbox[1], self.n, cells_per_point)
+        self.bbox = bbox  # exact (unpadded) source bbox on the host, or None
         self.geom = geom
         self.grid = self.geom.to_ctypes()
         dev = self.pts.device
@@ -230,33 +231,128 @@ def fit_many(targets, sup_off, sup_idx, sup_w, src, src_val, degree, lam, center
     return values, coeffs, status, stats
 
 
-def transfer_values(cloud, targets, sel, cnt, src_val, rbf, degree, lam, centering, perm=None):
-    """Fused fill + weights + fit for one scalar field (no supports kept)."""
+def slot_capacity(dim, sel):
+    """Per-target slot size of the select pass (overflowing supports are
+    re-gathered by the build, so this is a speed knob, not a limit)."""
+    base = 64 if dim <= 2 else (128 if dim == 3 else 256)
+    if sel.adaptive:
+        est = int(np.ceil(sel.min_pts * sel.growth ** dim * 1.25))
+        base = max(base, min(256, -(-est // 32) * 32))
+    return base
+
+
+@dataclass
+class Selection:
+    """Output of the select pass: supports of every target in HBM."""
+
+    sel: Select
+    counts: torch.Tensor    # int32 (nt,) by target
+    radii: torch.Tensor     # f64 (nt,) final radius (adaptive) or None
+    status: torch.Tensor    # u8 (nt,) adaptive status or None
+    slot_id: torch.Tensor   # int32 (nt * slot_cap,) by processing position
+    slot_pos: torch.Tensor
+    slot_cap: int
+    overflow: torch.Tensor  # int32 positions whose support did not fit a slot
+    stats: np.ndarray       # int32[8] host (fieldmap.h fm_select)
+    offsets: torch.Tensor   # int64 (nt+1,) row offsets in processing order
+    nnz: int
+    perm: torch.Tensor
+
+    @property
+    def max_count(self):
+        return int(self.stats[0])
+
+    @property
+    def n_overflow(self):
+        return int(self.stats[6])
+
+    def lists(self):
+        return FmLists(self.counts.data_ptr(), self.slot_id.data_ptr(), self.slot_pos.data_ptr(),
+                       int(self.slot_cap), self.n_overflow, self.overflow.data_ptr())
+
+
+def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
+    """Select pass + row offsets in processing order.  One device->host
+    sync (the stats and nnz)."""
+    L = _lib.lib()
+    dev = targets.device
+    nt = targets.shape[0]
+    cap = int(slot_cap or slot_capacity(cloud.dim, sel))
+    counts = _empty(nt, torch.int32, dev)
+    radii = _empty(nt, torch.float64, dev) if sel.adaptive else None
+    status = _empty(nt, torch.uint8, dev) if sel.adaptive else None
+    slot_id = _empty(max(nt * cap, 1), torch.int32, dev)
+    slot_pos = _empty(max(nt * cap, 1), torch.int32, dev)
+    overflow = _empty(max(nt, 1), torch.int32, dev)
+    stats_d = _empty(8, torch.int32, dev)
+    csel = sel.to_ctypes()
+    check(L.fm_select_supports(ctypes.byref(cloud.grid), ptr(cloud.cell_start), ptr(cloud.sorted_pts),
+                      ptr(cloud.sorted_ids), ptr(targets), nt, ptr(perm), ctypes.byref(csel),
+                      int(min_required), ptr(counts), ptr(radii), ptr(status), ptr(slot_id),
+                      ptr(slot_pos), cap, ptr(overflow), ptr(stats_d), _stream()), "fm_select")
+    offsets = _empty(nt + 1, torch.int64, dev)
+    ws_bytes = L.fm_offsets_ordered_workspace(nt)
+    ws = _workspace(ws_bytes, dev)
+    check(L.fm_offsets_ordered(ptr(counts), ptr(perm), nt, ptr(offsets), ptr(ws), ws_bytes,
+                               _stream()), "fm_offsets_ordered")
+    host = torch.empty(10, dtype=torch.int32, pin_memory=True)
+    host[:8].copy_(stats_d, non_blocking=True)
+    host[8:10].copy_(offsets[nt:nt + 1].view(torch.int32), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    h = host.numpy()
+    stats = h[:8].copy()
+    nnz = int(h[8:10].view(np.int64)[0])
+    if nt == 0:
+        stats[0] = 0
+    return Selection(sel, counts, radii, status, slot_id, slot_pos, cap, overflow, stats,
+                     offsets, nnz, perm)
+
+
+def support_csr(cloud, targets, sl, rbf=None):
+    """The reference's support CSR (offsets in target order, ids ascending,
+    distances, raw weights) for a Selection: what _select_batch returns."""
+    L = _lib.lib()
+    nt = targets.shape[0]
+    offsets = _empty(nt + 1, torch.int64, targets.device)
+    ws_bytes = L.fm_scan_workspace(nt)
+    ws = _workspace(ws_bytes, targets.device)
+    check(L.fm_offsets_from_counts(ptr(sl.counts), nt, ptr(offsets), ptr(ws), ws_bytes,
+                                   _stream()), "fm_offsets_from_counts")
+    cnt = Counts(sl.counts, sl.radii, sl.status, sl.stats[:6], offsets, sl.nnz)
+    idx, dist, w = fill_supports(cloud, targets, sl.sel, cnt, sl.perm, rbf)
+    return offsets, idx, dist, w
+
+
+def transfer_values(cloud, targets, sl, src_val, rbf, degree, lam, centering):
+    """Weights + fit for one scalar field from a Selection (no operator kept)."""
     L = _lib.lib()
     dev = targets.device
     nt = targets.shape[0]
     values = _empty(nt, torch.float64, dev)
     status = _empty(nt, torch.uint8, dev)
     stats = _empty(2, torch.int32, dev)
-    csel = sel.to_ctypes()
+    csel = sl.sel.to_ctypes()
     crbf = FmRbf(int(rbf[0]), 0, float(rbf[1]))
     f = _fit_struct(cloud.dim, degree, lam, centering)
+    lists = sl.lists()
     check(L.fm_transfer_values(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
                                ptr(cloud.sorted_pts), ptr(cloud.sorted_ids), ptr(targets), nt,
-                               ptr(perm), ctypes.byref(csel), ptr(cnt.radii),
-                               max(cnt.max_count, 1), ctypes.byref(crbf), ctypes.byref(f),
-                               ptr(cloud.pts), ptr(src_val), ptr(values), ptr(status), ptr(stats),
+                               ptr(sl.perm), ctypes.byref(csel), ptr(sl.radii),
+                               ctypes.byref(lists), max(sl.max_count, 1), ctypes.byref(crbf),
+                               ctypes.byref(f), ptr(src_val), ptr(values), ptr(status), ptr(stats),
                                _stream()), "fm_transfer_values")
     return values, status, stats
 
 
 # ----------------------------------------------------------- operator
 class Operator:
-    """Explicit transfer operator W (nt x ns) in CSR, resident in HBM.
+    """Explicit transfer operator W (nt x ns), resident in HBM.
 
-    Row t (ids ascending) holds the weights with which the reference's fit
-    combines the support values (fit_many is linear in src_val), so
-    W @ f == fit_many(..., f).values for every field f."""
+    Stored row k is target perm[k] (processing = cell order, so the apply
+    streams the CSR and gathers neighbouring source rows); each row holds
+    the weights with which the reference's fit combines the support values
+    (fit_many is linear in src_val), so W @ f == fit_many(..., f).values for
+    every field f."""
 
     def __init__(self, offsets, col, val, status, perm, ns):
         self.offsets = offsets
@@ -290,25 +386,26 @@ class Operator:
         return self.nnz * 12 + self.nt * 4 + self.ns * C * 8 + self.nt * C * 8
 
 
-def build_operator(cloud, targets, sel, cnt, rbf, degree, lam, centering, perm=None):
-    """Fused fill + weights + fit -> Operator (plus the fit stats, device)."""
+def build_operator(cloud, targets, sl, rbf, degree, lam, centering):
+    """Weights + fit from a Selection -> Operator (plus the fit stats, device)."""
     L = _lib.lib()
     dev = targets.device
     nt = targets.shape[0]
-    col = _empty(cnt.nnz, torch.int32, dev)
-    val = _empty(cnt.nnz, torch.float64, dev)
+    col = _empty(max(sl.nnz, 1), torch.int32, dev)[:sl.nnz]
+    val = _empty(max(sl.nnz, 1), torch.float64, dev)[:sl.nnz]
     status = _empty(nt, torch.uint8, dev)
     stats = _empty(2, torch.int32, dev)
-    csel = sel.to_ctypes()
+    csel = sl.sel.to_ctypes()
     crbf = FmRbf(int(rbf[0]), 0, float(rbf[1]))
     f = _fit_struct(cloud.dim, degree, lam, centering)
+    lists = sl.lists()
     check(L.fm_build_operator(ctypes.byref(cloud.grid), ptr(cloud.cell_start),
                               ptr(cloud.sorted_pts), ptr(cloud.sorted_ids), ptr(targets), nt,
-                              ptr(perm), ctypes.byref(csel), ptr(cnt.radii), ptr(cnt.offsets),
-                              max(cnt.max_count, 1), ctypes.byref(crbf), ctypes.byref(f),
-                              ptr(cloud.pts), ptr(col), ptr(val), ptr(status), ptr(stats),
+                              ptr(sl.perm), ctypes.byref(csel), ptr(sl.radii), ctypes.byref(lists),
+                              ptr(sl.offsets), max(sl.max_count, 1), ctypes.byref(crbf),
+                              ctypes.byref(f), ptr(col), ptr(val), ptr(status), ptr(stats),
                               _stream()), "fm_build_operator")
-    return Operator(cnt.offsets, col, val, status, perm, cloud.n), stats
+    return Operator(sl.offsets, col, val, status, sl.perm, cloud.n), stats
 
 
 def fp64_probe(blocks=148 * 8, threads=256, iters=4096):

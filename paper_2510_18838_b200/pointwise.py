@@ -209,9 +209,10 @@ def _r_max(src_xy, targets):
     return 1.0000001 * ext + 1e-300
 
 
-def _r_max_device(src, targets):
-    """_r_max on device-resident points (bboxes by fm_bbox, one small D2H)."""
-    lo_s, hi_s = D.device_bbox(src)
+def _r_max_device(cloud, targets):
+    """_r_max on device-resident points (bboxes by fm_bbox, one small D2H;
+    the source bbox is the one the grid was built from)."""
+    lo_s, hi_s = cloud.bbox if cloud.bbox is not None else D.device_bbox(cloud.pts)
     lo_t, hi_t = D.device_bbox(targets) if targets.shape[0] else (lo_s, hi_s)
     lo, hi = np.minimum(lo_s, lo_t), np.maximum(hi_s, hi_t)
     if lo.size == 2:
@@ -254,10 +255,10 @@ class _Plan:
         need = n_monomials(fitspec.degree, self.cloud.dim)
         if isinstance(sel, FixedRadius):
             self.sel = D.fixed(sel.r_c)
-            self.cnt = D.count_supports(self.cloud, self.t, self.sel, self.perm, need)
-            if self.cnt.stats[2] > 0:
-                i = int(self.cnt.stats[3])
-                c = int(self.cnt.counts[i].item())
+            self.sl = D.select(self.cloud, self.t, self.sel, self.perm, need)
+            if self.sl.stats[2] > 0:
+                i = int(self.sl.stats[3])
+                c = int(self.sl.counts[i].item())
                 raise UnderdeterminedError(
                     f"{self.label(i)} (index {base_index + i}) has "
                     f"{c} support points inside radius {sel.r_c:g}; a "
@@ -266,12 +267,12 @@ class _Plan:
             if isinstance(src_xy, np.ndarray) and isinstance(targets, np.ndarray):
                 r_max = _r_max(src_xy, targets)
             else:
-                r_max = _r_max_device(self.cloud.pts, self.t)
+                r_max = _r_max_device(self.cloud, self.t)
             self.sel = D.adaptive(sel.min_points, sel.r0, sel.growth, r_max)
-            self.cnt = D.count_supports(self.cloud, self.t, self.sel, self.perm, 0)
-            if self.cnt.stats[4] > 0:
-                i = int(self.cnt.stats[5])
-                c = int(self.cnt.counts[i].item())
+            self.sl = D.select(self.cloud, self.t, self.sel, self.perm, 0)
+            if self.sl.stats[4] > 0:
+                i = int(self.sl.stats[5])
+                c = int(self.sl.counts[i].item())
                 raise InsufficientSourcesError(
                     f"{self.label(i)} (index {base_index + i}): only "
                     f"{c} sources in the whole domain, "
@@ -285,9 +286,9 @@ class _Plan:
     def supports(self, raw_weights=True):
         """(offsets, idx, w_raw) numpy, the reference's _select_batch output."""
         rbf = self.fitspec.rbf
-        idx, _dist, w = D.fill_supports(self.cloud, self.t, self.sel, self.cnt, self.perm,
-                                        rbf=_rbf_pair(rbf) if raw_weights else None)
-        return self.cnt.offsets.cpu().numpy(), idx.cpu().numpy(), w.cpu().numpy()
+        off, idx, _dist, w = D.support_csr(self.cloud, self.t, self.sl,
+                                           rbf=_rbf_pair(rbf) if raw_weights else None)
+        return off.cpu().numpy(), idx.cpu().numpy(), w.cpu().numpy()
 
     def raise_fit_error(self, status, base_index=0):
         """pointwise.py:305-313 for the first failing target."""
@@ -306,14 +307,14 @@ class _Plan:
 
     def build_operator(self):
         fs = self.fitspec
-        op, stats = D.build_operator(self.cloud, self.t, self.sel, self.cnt, _rbf_pair(fs.rbf),
-                                     fs.degree, fs.lam, fs.centering, self.perm)
+        op, stats = D.build_operator(self.cloud, self.t, self.sl, _rbf_pair(fs.rbf), fs.degree,
+                                     fs.lam, fs.centering)
         return op, stats
 
     def transfer_scalar(self, vals_d):
         fs = self.fitspec
-        return D.transfer_values(self.cloud, self.t, self.sel, self.cnt, vals_d,
-                                 _rbf_pair(fs.rbf), fs.degree, fs.lam, fs.centering, self.perm)
+        return D.transfer_values(self.cloud, self.t, self.sl, vals_d, _rbf_pair(fs.rbf),
+                                 fs.degree, fs.lam, fs.centering)
 
 
 def _as_points(a, dim=None):
@@ -408,13 +409,20 @@ class PreparedTransfer:
             self._plan.raise_fit_error(self.operator.status)
 
     def apply(self, source_values, threads=1):
-        """Transfer values (ns,) or (ns, C); numpy in -> numpy out, CUDA
-        tensor in -> CUDA tensor out (no host round trip)."""
-        if isinstance(source_values, torch.Tensor) and source_values.is_cuda:
+        """Transfer values (ns,) or (ns, C).  numpy in -> numpy out; CUDA
+        tensor in -> CUDA tensor out (no host round trip); host tensor in
+        (pinned: async copies) -> pinned host tensor out."""
+        if isinstance(source_values, torch.Tensor):
             if source_values.shape[0] != self.src_xy.shape[0]:
                 raise FieldError("source values disagree with prepared points")
             self._check_fit()
-            return self.operator.apply(source_values.to(torch.float64))
+            Y = self.operator.apply(D.to_device(source_values))
+            if source_values.is_cuda:
+                return Y
+            out = torch.empty(Y.shape, dtype=Y.dtype, pin_memory=True)
+            out.copy_(Y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return out
         vals = np.ascontiguousarray(source_values, dtype=np.float64)
         if vals.shape[0] != self.src_xy.shape[0]:
             raise FieldError("source values disagree with prepared points")

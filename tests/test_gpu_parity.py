@@ -236,17 +236,25 @@ def test_fit_many_variants_vs_reference(deg, lam, cen):
     key = f"d{deg}_l{'r' if lam else '0'}_{'c' if cen else 'u'}"
     assert np.array_equal(st, g["fit_s_" + key])
     assert _rel(v, g["fit_v_" + key]) < VALUE_RTOL
-    # coefficients: relative to the coefficient scale of each target
+    # coefficients in the solver's scaled basis (c_j * s^deg_j, _ext.pyx:411-412):
+    # both solvers are backward stable there, so they agree to ~eps*cond(A)
     want_c = g["fit_c_" + key]
-    scale = np.abs(want_c).max(axis=1, keepdims=True)
-    assert np.max(np.abs(c - want_c) / scale) < 1e-9
+    s = np.empty(n)
+    for i in range(n):
+        d = src[idx[off[i]:off[i + 1]]] - (tg[i] if cen else 0.0)
+        s[i] = np.sqrt(np.max(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]))
+    degs = np.array([0, 1, 1, 2, 2, 2])[:c.shape[1]]
+    sp = s[:, None] ** degs[None, :]
+    scale = np.abs(want_c * sp).max(axis=1, keepdims=True)
+    # uncentered fits at C1 geometry have cond(A) up to ~4e8
+    assert np.max(np.abs((c - want_c) * sp) / scale) < (1e-9 if cen else 1e-6)
 
 
 def test_singular_status_outside_gray_zone():
     g = golden("singular")
     off = g["off"]
     n = len(g["degs"])
-    gray = 0
+    gray = compared = 0
     for i in range(n):
         sl = slice(off[i], off[i + 1])
         m = off[i + 1] - off[i]
@@ -257,9 +265,12 @@ def test_singular_status_outside_gray_zone():
             gray += 1
             continue
         assert st[0] == g["status"][i], (i, cond)
-        if st[0] == 0 and cond < 1e6:
+        # value parity is meaningful only for well-posed fits: two backward
+        # stable solvers differ by ~eps*cond(A) (SURVEY.md §7 "Rank / status parity")
+        if st[0] == 0 and cond < 1e5:
+            compared += 1
             assert abs(v[0] - g["values"][i]) <= VALUE_RTOL * abs(g["values"][i]) + 1e-13
-    assert gray < n // 2
+    assert gray < n // 2 and compared >= 15
 
 
 # ------------------------------------------------- transfers (a8, a9)
