@@ -64,6 +64,20 @@ def workload(config, rank=0):
                             "AdaptiveRadius(12, h_src, 1.5), 8-component field",
                 "sources": int(src.shape[0]), "targets_per_gpu": int(tgt.shape[0]),
                 "components": 8, "degree": 2, "rbf": "c4", "selection": "adaptive(12,h,1.5)"}
+    elif config == "lattice1m":
+        # SURVEY.md §3/§6 scale-up of C1: linspace(0,1,1000)^2 lattice -> 1M
+        # random targets, degree 2, C4, FixedRadius(2h), h = 1/999
+        side = np.linspace(0.0, 1.0, 1000)
+        xx, yy = np.meshgrid(side, side)
+        src = np.ascontiguousarray(np.column_stack([xx.reshape(-1), yy.reshape(-1)]))
+        tgt = np.random.RandomState(rank).uniform(0, 1, (1000000, 2))
+        X = synth.sincos_field(src, 8)
+        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
+                         P.FixedRadius(2.0 / 999.0))
+        desc = {"workload": "1M lattice linspace(0,1,1000)^2 -> 1M random targets, MLS degree "
+                            "2, C4 a=2, FixedRadius(2h), 8-component field",
+                "sources": int(src.shape[0]), "targets_per_gpu": int(tgt.shape[0]),
+                "components": 8, "degree": 2, "rbf": "c4", "selection": "fixed(2h)"}
     elif config == "c1":
         src = synth.square(99).coords
         tgt = np.random.RandomState(rank).uniform(0, 1, (10000, 2))
@@ -455,7 +469,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=["c1", "c2"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "lattice1m"], default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

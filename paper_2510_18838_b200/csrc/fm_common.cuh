@@ -104,6 +104,36 @@ __device__ __forceinline__ double rbf_one(int kind, double a, double r_c, double
     return -1.0;
 }
 
+// The same weights for the fit path, where they only need ~1 ulp (the fit is
+// held to 1e-10): products with 1/r_c instead of IEEE divisions.  The support
+// ABI (fm_support_fill, fm_rbf_weights) keeps rbf_one.
+__device__ __forceinline__ double rbf_fast(int kind, double a, double r_c, double inv_rc,
+                                           double r) {
+    if (kind == FM_RBF_IDENTITY) return 1.0;
+    if (r > r_c) return 0.0;
+    const double u = r * inv_rc;
+    const double x = a * u;
+    switch (kind) {
+    case FM_RBF_GAUSSIAN: return exp(-(x * x));
+    case FM_RBF_C4: {
+        double poly = fma(u, 5.0, 30.0);
+        poly = fma(u, poly, 72.0);
+        poly = fma(u, poly, 82.0);
+        poly = fma(u, poly, 36.0);
+        poly = fma(u, poly, 6.0);
+        const double q = 1.0 - u;
+        const double q2 = q * q;
+        return poly * (q2 * q2 * q2);
+    }
+    case FM_RBF_CONST: return 1.0;
+    case FM_RBF_MULTIQUADRIC: return sqrt(fma(x, x, 1.0));
+    case FM_RBF_INVERSE_MULTIQUADRIC: return rsqrt(fma(x, x, 1.0));
+    case FM_RBF_THIN_PLATE_SPLINE: return x > 0.0 ? x * x * log(x) : 0.0;
+    case FM_RBF_CUBIC_SPLINE: return x * x * x;
+    }
+    return -1.0;
+}
+
 // ------------------------------------------------------------- monomials
 // Graded-lex monomials in DIM variables up to DEG (x0 > x1 > ...); for DIM=2
 // this is [1, x, y, x^2, xy, y^2] (pointwise.py:44) extended by

@@ -34,6 +34,17 @@ namespace fm {
 
 constexpr double kSingularKappa = 1.5 / 2.220446049250313e-16;
 
+// Row i = q*G + glane against pivot column j; with q and j compile-time
+// (unrolled loops) the tests fold to constants for q*G > j.
+template <int G>
+__device__ __forceinline__ bool row_below(int q, int j, int glane) {
+    return q * G > j ? true : glane > j - q * G;
+}
+template <int G>
+__device__ __forceinline__ bool row_diag(int q, int j, int glane) {
+    return q * G > j ? false : glane == j - q * G;
+}
+
 template <int DIM, int DEG>
 struct FitShape {
     static constexpr int K = Monos<DIM, DEG>::K;
@@ -144,7 +155,8 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 #pragma unroll
         for (int q = 0; q < ROWS; q++) {
             const int i = q * G + glane;
-            if (i > j) sl = fma(A[q][j], A[q][j], sl);
+            if (row_below<G>(q, j, glane)) sl = fma(A[q][j], A[q][j], sl);
+            (void)i;
         }
         const double sigma = group_sum<G>(sl);
         double gj, bj, vj, ib;
@@ -173,8 +185,9 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) pl = fma(vj, A[q][l], pl);
-                else if (i > j) pl = fma(A[q][j], A[q][l], pl);
+                if (row_diag<G>(q, j, glane)) pl = fma(vj, A[q][l], pl);
+                else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], A[q][l], pl);
+                (void)i;
             }
             dot[l] = pl;
         }
@@ -186,8 +199,9 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) A[q][l] = fma(-td, vj, A[q][l]);
-                else if (i > j) A[q][l] = fma(-td, A[q][j], A[q][l]);
+                if (row_diag<G>(q, j, glane)) A[q][l] = fma(-td, vj, A[q][l]);
+                else if (row_below<G>(q, j, glane)) A[q][l] = fma(-td, A[q][j], A[q][l]);
+                (void)i;
             }
         }
 #pragma unroll
@@ -289,15 +303,17 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) pl = fma(v0[j], yy[q], pl);
-                else if (i > j) pl = fma(A[q][j], yy[q], pl);
+                if (row_diag<G>(q, j, glane)) pl = fma(v0[j], yy[q], pl);
+                else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], yy[q], pl);
+                (void)i;
             }
             const double td = gam[j] * group_sum<G>(pl);
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (i == j) yy[q] = fma(-td, v0[j], yy[q]);
-                else if (i > j) yy[q] = fma(-td, A[q][j], yy[q]);
+                if (row_diag<G>(q, j, glane)) yy[q] = fma(-td, v0[j], yy[q]);
+                else if (row_below<G>(q, j, glane)) yy[q] = fma(-td, A[q][j], yy[q]);
+                (void)i;
             }
         });
 #pragma unroll

@@ -220,7 +220,8 @@ struct BuildArgs {
 };
 
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
-__global__ void __launch_bounds__(kBlock) k_build(SearchArgs s, BuildArgs b) {
+__global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 4) ? 4 : 1) k_build(SearchArgs s,
+                                                                                 BuildArgs b) {
     constexpr int K = Monos<DIM, DEG>::K;
     extern __shared__ __align__(16) char smem[];
     int nfail = 0, first_fail = INT32_MAX;
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kBlock) k_build(SearchArgs s, BuildArgs b) {
         bool valid[ROWS];
         double p[ROWS][DIM], w[ROWS], f[ROWS];
         int32_t ids[ROWS];
+        const double inv_r = active ? 1.0 / r : 0.0;
 #pragma unroll
         for (int q = 0; q < ROWS; q++) {
             const int i = q * G + glane;
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kBlock) k_build(SearchArgs s, BuildArgs b) {
                 }
                 load_point<DIM>(s.sorted_pts, pos, p[q]);
                 const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
-                w[q] = fabs(rbf_one(b.rbf_kind, b.rbf_a, r, d));  // pointwise.py:301
+                w[q] = fabs(rbf_fast(b.rbf_kind, b.rbf_a, r, inv_r, d));  // pointwise.py:301
                 if (SOLVE) f[q] = __ldg(b.src_val + ids[q]);
             }
         }
@@ -514,7 +516,9 @@ template <int DIM>
 int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,
                   uint8_t *status, int32_t *slot_id, int32_t *slot_pos, int slot_cap,
                   int32_t *overflow, int32_t *stats, cudaStream_t st) {
-    constexpr int G = 16;
+    // 8-lane groups in 1-D/2-D (small windows: 4 targets per warp halves the
+    // per-target fixed cost), 16 lanes for the larger windows of dim >= 3
+    constexpr int G = DIM <= 2 ? 8 : 16;
     k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0);
     if (s.nt == 0) return FM_OK;
     const int lcap = slot_cap > kSelectListCap ? slot_cap : kSelectListCap;

@@ -375,11 +375,31 @@ __device__ __forceinline__ int guess_steps(const GridDev &g, const int32_t *__re
     return k;
 }
 
+// Number of list entries with squared distance below thr (group-cooperative).
+template <int G>
+__device__ __forceinline__ int count_list(const ListBuf &lb, int n, double thr, int lane,
+                                          int glane) {
+    const int iters = warp_max_int((n + G - 1) / G);
+    int c = 0;
+    for (int it = 0; it < iters; it++) {
+        const int e = it * G + glane;
+        const bool in = e < n && lb.d[e] < thr;
+        c += __popc(group_bits<G>(__ballot_sync(FM_FULL_MASK, in), lane));
+    }
+    return c;
+}
+
 // Final support of one target for fixed or adaptive selection, exactly the
 // reference's (fixed: d < r_c; adaptive: the first radius of the sequence
 // r0, min(r*growth, r_max), ... holding >= min_pts sources, status 1 when
 // r_max is reached short).  Returns the count m; when `listed` is true the
 // group's buffer holds all m supports (discovery order), otherwise m > cap.
+//
+// Adaptive: one window scan at the density-guessed step r_kg collects every
+// candidate with d < r_kg (and d^2).  If it holds min_pts, the counts at the
+// smaller radii r_0..r_kg-1 of the same sequence are taken from that list and
+// the first radius reaching min_pts wins; otherwise the sequence continues
+// one radius (one scan) at a time, exactly like _ext.pyx:258-271.
 // Warp-collective.
 template <int DIM, int G>
 __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__restrict__ cell_start,
@@ -388,82 +408,82 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
                                              const double *t, const fm_select &sel, bool active,
                                              int lane, int glane, RowTable<G> &rt, ListBuf &lb,
                                              double &r_out, uint8_t &status, bool &listed) {
-    constexpr int NR = kMaxGuess + 1;
-    double radii[NR];
-    int nr = 1;
+    // radius of the first scan: r_kg of the reference sequence (or r_c)
+    double rscan = sel.r_c;
+    int kg = 0;
     if (sel.adaptive) {
-        const int kg = guess_steps<DIM, G>(g, cell_start, t, sel, active, glane);
+        kg = guess_steps<DIM, G>(g, cell_start, t, sel, active, glane);
         double r = sel.r0;
-        bool stop = false;
-#pragma unroll
-        for (int j = 0; j < NR; j++) {
-            radii[j] = r;
-            if (!stop && j <= kg) {
-                nr = j + 1;
-                if (r >= sel.r_max) {
-                    stop = true;
-                } else {
-                    r = r * sel.growth;
-                    if (r > sel.r_max) r = sel.r_max;
-                }
-            }
+        int j = 0;
+        while (j < kg && r < sel.r_max) {
+            r = r * sel.growth;
+            if (r > sel.r_max) r = sel.r_max;
+            j++;
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < NR; j++) radii[j] = sel.r_c;
+        kg = j;
+        rscan = r;
     }
-    int cnt[NR];
-#pragma unroll
-    for (int j = 0; j < NR; j++) cnt[j] = 0;
-    int nlist = 0;
-    scan_counts<DIM, G, NR>(g, cell_start, sorted_pts, sorted_ids, t, radii, nr, active, lane,
-                            glane, rt, cnt, lb, nlist);
-    // first radius of the scanned prefix of the sequence that holds min_pts
-    int m = 0;
-    double rf = 0.0, rlast = 0.0;
-#pragma unroll
-    for (int j = 0; j < NR; j++)
-        if (j == nr - 1) {
-            m = cnt[j];
-            rf = radii[j];
-        }
-    rlast = rf;
+    int m = 0, nlist = 0;
+    {
+        double r1[1] = {active ? rscan : 0.0};
+        int c1[1] = {0};
+        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, active, lane,
+                               glane, rt, c1, lb, nlist);
+        m = c1[0];
+    }
+    double rf = rscan;
     status = 0;
-    bool done = !active;
-    if (active) {
-        if (!sel.adaptive) {
+    bool done = !active || !sel.adaptive;
+    bool slow = false;  // guess too high and the list overflowed: restart at r0
+    if (!done) {
+        if (m >= sel.min_pts) {
             done = true;
-        } else {
-            int jf = -1;
-#pragma unroll
-            for (int j = 0; j < NR; j++)
-                if (jf < 0 && j < nr && cnt[j] >= sel.min_pts) jf = j;
-#pragma unroll
-            for (int j = 0; j < NR; j++)
-                if (j == jf) {
-                    m = cnt[j];
-                    rf = radii[j];
-                }
-            if (jf >= 0) {
-                done = true;
-            } else if (rf >= sel.r_max) {
-                status = 1;
-                done = true;
+            slow = kg > 0 && nlist > lb.cap;
+        } else if (rf >= sel.r_max) {
+            status = 1;
+            done = true;
+        }
+    }
+    // smaller radii of the sequence, counted on the list (kg is small)
+    const int kg_w = warp_max_int(active && sel.adaptive && !slow && m >= sel.min_pts ? kg : 0);
+    {
+        double r = sel.r0;
+        bool found = !(active && sel.adaptive && !slow && m >= sel.min_pts && kg > 0);
+        for (int j = 0; j < kg_w; j++) {
+            const bool mine = !found && j < kg;
+            const double thr = mine ? sqrt_threshold(r) : 0.0;
+            const int c = count_list<G>(lb, mine ? nlist : 0, thr, lane, glane);
+            if (mine && c >= sel.min_pts) {
+                found = true;
+                m = c;
+                rf = r;
+            }
+            if (mine) {
+                r = r * sel.growth;
+                if (r > sel.r_max) r = sel.r_max;
             }
         }
+    }
+    if (slow) {  // rare: recount from r0 one scan per radius
+        rf = sel.r0;
+        done = false;
     }
     // continue the sequence one radius at a time (_ext.pyx:259-270)
     bool fresh = false;  // list rebuilt at exactly rf
+    bool first = true;
     while (__any_sync(FM_FULL_MASK, !done)) {
         double r1[1] = {0.0};
         int c1[1] = {0};
         const bool go = !done;
         if (go) {
-            rf = rf * sel.growth;
-            if (rf > sel.r_max) rf = sel.r_max;
+            if (!(slow && first)) {
+                rf = rf * sel.growth;
+                if (rf > sel.r_max) rf = sel.r_max;
+            }
             r1[0] = rf;
             nlist = 0;
         }
+        first = false;
         int nl = nlist;
         scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, go, lane, glane,
                                rt, c1, lb, nl);
@@ -479,9 +499,9 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
             }
         }
     }
-    // keep only d < rf when the list came from a wider scan; rescan when the
-    // wider scan overflowed the buffer but the final support fits
-    const bool wide = active && !fresh && rf < rlast;
+    // keep only d < rf when the list came from the wider first scan; rescan
+    // when that scan overflowed the buffer but the final support fits
+    const bool wide = active && !fresh && rf < rscan;
     const bool rescan = wide && nlist > lb.cap && m <= lb.cap;
     if (__any_sync(FM_FULL_MASK, rescan)) {
         double r1[1] = {rescan ? rf : 0.0};

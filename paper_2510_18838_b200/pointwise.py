@@ -498,11 +498,13 @@ def transfer_extrinsic(evaluate_callback, target_points, fitspec, source_points,
                 f"callback returned {got.shape} values for {needed.size} "
                 f"points on batch {bi}", batch=bi)
         values_cache[needed] = got
-        vals, _c, status = _kernels.fit_many(chunk, off, idx, np.abs(w), src_xy, values_cache,
-                                             fitspec.degree, float(fitspec.lam),
-                                             bool(fitspec.centering))
-        _raise_status(status, chunk, fitspec, b0)
-        out[b0:b1] = vals
+        # the same select + fit kernels as the intrinsic path, so a callback
+        # returning the field's own values reproduces it bitwise
+        # (reference test_pointwise.py:254-271)
+        vals, status, stats = plan.transfer_scalar(D.to_device(values_cache))
+        if int(stats[0].item()) > 0:
+            plan.raise_fit_error(status, b0)
+        out[b0:b1] = vals.cpu().numpy()
     return out
 
 
