@@ -195,13 +195,16 @@ int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int6
  * chosen radius is still the first of that exact sequence holding min_pts.
  * Targets whose support exceeds slot_cap are appended (as positions k) to
  * overflow[]; the build re-gathers them.  stats (device int32[8], written
- * by the call): fm_support_count's 6 entries, [6] #overflow, [7] 0. */
+ * by the call): fm_support_count's 6 entries, [6] #overflow, [7] 0.
+ * pos_info (16 B per position: int32 target, int32 support size, f64 radius)
+ * and pos_targets (dim doubles per position) are optional per-position
+ * copies that let the build read everything by position (may be NULL). */
 int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                        const int32_t *sorted_ids, const double *targets, int64_t nt,
                        const int32_t *perm, const fm_select *sel, int32_t min_required,
                        int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
                        int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
-                       fm_stream_t stream);
+                       void *pos_info, double *pos_targets, fm_stream_t stream);
 
 /* Row offsets of an operator stored in processing order:
  * offsets[k+1] = offsets[k] + counts[perm[k]] (perm may be NULL). */
@@ -218,6 +221,8 @@ typedef struct fm_lists {
     int32_t slot_cap;
     int32_t n_overflow;
     const int32_t *overflow;
+    const void *pos_info;       /* optional, from fm_select_supports */
+    const double *pos_targets;  /* optional, from fm_select_supports */
 } fm_lists;
 
 /* --------------------------------- a8/a13: transfer operator (new)

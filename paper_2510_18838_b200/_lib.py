@@ -47,7 +47,8 @@ class FmFit(ctypes.Structure):
 
 class FmLists(ctypes.Structure):
     _fields_ = [("counts", c_vp), ("slot_id", c_vp), ("slot_pos", c_vp), ("slot_cap", c_i32),
-                ("n_overflow", c_i32), ("overflow", c_vp)]
+                ("n_overflow", c_i32), ("overflow", c_vp), ("pos_info", c_vp),
+                ("pos_targets", c_vp)]
 
 
 P = ctypes.POINTER
@@ -70,8 +71,9 @@ SIGNATURES = {
     "fm_rbf_weights": (c_i32, [c_i32, c_dbl, c_dbl, c_vp, c_i64, c_vp, c_vp]),
     "fm_fit_many": (c_i32, [P(FmFit), c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                             c_vp, c_vp, c_vp, c_vp]),
-    "fm_select_supports": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect), c_i32,
-                          c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "fm_select_supports": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
+                                   c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp]),
     "fm_offsets_ordered_workspace": (c_sz, [c_i64]),
     "fm_offsets_ordered": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "fm_build_operator": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),

@@ -338,6 +338,8 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
         b.slot_pos = lists->slot_pos;
         b.slot_cap = lists->slot_cap;
         b.counts = lists->counts;
+        b.pos_info = reinterpret_cast<const PosInfo *>(lists->pos_info);
+        b.pos_t = lists->pos_targets;
         const int mm = max_count < lists->slot_cap ? max_count : lists->slot_cap;
         rc = dispatch_build(grid->dim, fit->degree, solve, true, s, b, mm, st);
         if (rc || lists->n_overflow == 0) return rc;
@@ -376,7 +378,7 @@ int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const dou
                        const int32_t *perm, const fm_select *sel, int32_t min_required,
                        int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
                        int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
-                       fm_stream_t stream) {
+                       void *pos_info, double *pos_targets, fm_stream_t stream) {
     if (!grid_ok(grid) || !sel || nt < 0 || slot_cap < 1 || !stats || !overflow || !counts)
         return FM_ERR_ARG;
     if (sel->adaptive ? !(sel->r0 > 0.0 && sel->growth > 1.0 && sel->min_pts >= 1 && radii)
@@ -385,12 +387,13 @@ int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const dou
     const SearchArgs s = make_search(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm,
                                      sel, nullptr);
     cudaStream_t st = (cudaStream_t)stream;
+    PosInfo *pi = reinterpret_cast<PosInfo *>(pos_info);
     switch (grid->dim) {
-    case 1: return dim1_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
-    case 2: return dim2_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
-    case 3: return dim3_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
-    case 4: return dim4_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
-    default: return dim5_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, st);
+    case 1: return dim1_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
+    case 2: return dim2_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
+    case 3: return dim3_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
+    case 4: return dim4_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
+    default: return dim5_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
     }
 }
 

@@ -14,6 +14,22 @@ namespace fm {
 
 constexpr int kBlock = 128;
 
+// Per processing position k, written by the select pass so the build's first
+// loads are indexed by k only (no perm -> target -> count chain):
+// (target id, support size, final radius).
+struct __align__(16) PosInfo {
+    int32_t tid;
+    int32_t m;
+    double r;
+};
+__device__ __forceinline__ PosInfo make_pos_info(int32_t tid, int32_t m, double r) {
+    PosInfo p;
+    p.tid = tid;
+    p.m = m;
+    p.r = r;
+    return p;
+}
+
 struct SearchArgs {
     GridDev g;
     const int32_t *cell_start;
@@ -206,6 +222,8 @@ struct BuildArgs {
     const int32_t *slot_pos;
     int slot_cap;
     const int32_t *counts;  // support size per target (FROM_SLOTS)
+    const PosInfo *pos_info;  // optional per-position (tid, m, r) from the select pass
+    const double *pos_t;      // optional per-position target coordinates
     const int64_t *offsets;
     int cap;  // rescan list capacity
     int rbf_kind;
@@ -234,13 +252,25 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 4) ? 4 : 1) k_build
         const int64_t ii = tile * GPW + lane / G;
         bool active = ii < b.nk;
         const int64_t k = active ? (b.klist ? (int64_t)b.klist[ii] : ii) : 0;
-        const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+        int64_t tid;
         double t[DIM];
-        load_target<DIM>(s.targets, tid, active, t);
-        const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
-        int m;
+        double r;
+        int m = 0;
+        if (FROM_SLOTS && b.pos_info) {
+            // per-position record of the select pass: loads indexed by k only
+            const PosInfo pi = active ? b.pos_info[k] : make_pos_info(0, 0, 0.0);
+            tid = pi.tid;
+            m = pi.m;
+            r = pi.r;
+#pragma unroll
+            for (int a = 0; a < DIM; a++) t[a] = active ? __ldg(b.pos_t + k * DIM + a) : 0.0;
+        } else {
+            tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+            load_target<DIM>(s.targets, tid, active, t);
+            r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
+            if (FROM_SLOTS) m = active ? b.counts[tid] : 0;
+        }
         if (FROM_SLOTS) {
-            m = active ? b.counts[tid] : 0;
             if (m > b.slot_cap) {  // overflow: built by the rescan launch
                 active = false;
                 m = 0;
@@ -323,7 +353,9 @@ __global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_req
                                                    int32_t *__restrict__ slot_id,
                                                    int32_t *__restrict__ slot_pos, int slot_cap,
                                                    int32_t *__restrict__ overflow,
-                                                   int32_t *__restrict__ stats) {
+                                                   int32_t *__restrict__ stats,
+                                                   PosInfo *__restrict__ pos_info,
+                                                   double *__restrict__ pos_t) {
     extern __shared__ __align__(16) char smem[];
     constexpr int GPW = 32 / G;
     const int grp = threadIdx.x / G;
@@ -356,15 +388,41 @@ __global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_req
                 // rank sort by id straight into the slot (ids are distinct)
                 int32_t *oid = slot_id + k * slot_cap;
                 int32_t *opos = slot_pos + k * slot_cap;
-                for (int e = glane; e < m; e += G) {
-                    const int32_t id = lb.id[e];
-                    int rank = 0;
-                    for (int f2 = 0; f2 < m; f2++) rank += lb.id[f2] < id;
-                    oid[rank] = id;
-                    opos[rank] = lb.pos[e];
+                // up to 4 entries per lane ranked against pairs of ids (LDS.64)
+                for (int e0 = 0; e0 < m; e0 += 4 * G) {
+                    int32_t myid[4];
+                    int rk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int e = e0 + u * G + glane;
+                        myid[u] = e < m ? lb.id[e] : INT32_MAX;
+                        rk[u] = 0;
+                    }
+                    for (int f2 = 0; f2 < m; f2 += 2) {
+                        const int2 two = *reinterpret_cast<const int2 *>(lb.id + f2);
+                        const int32_t second = f2 + 1 < m ? two.y : INT32_MAX;
+#pragma unroll
+                        for (int u = 0; u < 4; u++)
+                            rk[u] += (two.x < myid[u]) + (second < myid[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int e = e0 + u * G + glane;
+                        if (e < m) {
+                            oid[rk[u]] = myid[u];
+                            opos[rk[u]] = lb.pos[e];
+                        }
+                    }
                 }
             } else if (glane == 0) {
                 overflow[atomicAdd(stats + 6, 1)] = (int32_t)k;
+            }
+            if (pos_info && glane == 0)
+                pos_info[k] = make_pos_info((int32_t)tid, m, s.sel.adaptive ? r : s.sel.r_c);
+            if (pos_t && glane < DIM) {
+#pragma unroll
+                for (int a = 0; a < DIM; a++)
+                    if (a == glane) pos_t[k * DIM + a] = t[a];
             }
             if (glane == 0) {
                 counts[tid] = m;
@@ -515,7 +573,8 @@ constexpr int kSelectListCap = 128;  // per-group candidate list of the select p
 template <int DIM>
 int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,
                   uint8_t *status, int32_t *slot_id, int32_t *slot_pos, int slot_cap,
-                  int32_t *overflow, int32_t *stats, cudaStream_t st) {
+                  int32_t *overflow, int32_t *stats, PosInfo *pos_info, double *pos_t,
+                  cudaStream_t st) {
     // 8-lane groups in 1-D/2-D (small windows: 4 targets per warp halves the
     // per-target fixed cost), 16 lanes for the larger windows of dim >= 3
     constexpr int G = DIM <= 2 ? 8 : 16;
@@ -530,7 +589,7 @@ int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, do
                              (int)sm);
     k_select<DIM, G><<<grid_blocks(s.nt, kBlock / G, 16), kBlock, sm, st>>>(
         s, min_required, lcap, counts, radii, status, slot_id, slot_pos, slot_cap, overflow,
-        stats);
+        stats, pos_info, pos_t);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -613,7 +672,8 @@ int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const i
     int dim##N##_fill(const SearchArgs &, const int64_t *, int, int64_t *, double *, int,        \
                       double, double *, cudaStream_t);                                            \
     int dim##N##_select(const SearchArgs &, int32_t, int32_t *, double *, uint8_t *, int32_t *,  \
-                        int32_t *, int, int32_t *, int32_t *, cudaStream_t);
+                        int32_t *, int, int32_t *, int32_t *, PosInfo *, double *,            \
+                        cudaStream_t);
 #define FM_DECLARE_DEG(N, P)                                                                      \
     int dim##N##_deg##P##_build(bool, bool, const SearchArgs &, const BuildArgs &, int,          \
                                 cudaStream_t);                                                    \
@@ -643,8 +703,10 @@ FM_DECLARE_DEG(5, 0) FM_DECLARE_DEG(5, 1) FM_DECLARE_DEG(5, 2)
     }                                                                                              \
     int dim##N##_select(const SearchArgs &s, int32_t need, int32_t *c, double *r, uint8_t *st,    \
                         int32_t *sid, int32_t *spos, int scap, int32_t *ovf, int32_t *stats,       \
+                        PosInfo *pinfo, double *pt,                                                \
                         cudaStream_t stream) {                                                     \
-        return launch_select<N>(s, need, c, r, st, sid, spos, scap, ovf, stats, stream);           \
+        return launch_select<N>(s, need, c, r, st, sid, spos, scap, ovf, stats, pinfo, pt,       \
+                                stream);           \
     }
 
 #define FM_DEFINE_DEG(N, P)                                                                        \

@@ -267,13 +267,15 @@ struct ListBuf {
 __device__ __forceinline__ double sqrt_threshold(double r) {
     double x = mul_rn(r, r);
     if (!(x < INFINITY) || !(x > 0.0)) return x;
-    for (int it = 0; it < 64; it++) {  // step down while the predecessor still fails
+    if (__dsqrt_rn(x) < r) {
+        do {  // x passes: step up to the first failing double
+            x = __longlong_as_double(__double_as_longlong(x) + 1);
+        } while (__dsqrt_rn(x) < r);
+        return x;
+    }
+    for (int it = 0; it < 64; it++) {  // x fails: step down while the predecessor fails too
         const double xp = __longlong_as_double(__double_as_longlong(x) - 1);
         if (xp > 0.0 && __dsqrt_rn(xp) >= r) x = xp;
-        else break;
-    }
-    for (int it = 0; it < 64; it++) {  // step up while x still passes
-        if (__dsqrt_rn(x) < r) x = __longlong_as_double(__double_as_longlong(x) + 1);
         else break;
     }
     return x;

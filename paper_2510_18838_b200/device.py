@@ -257,6 +257,8 @@ class Selection:
     offsets: torch.Tensor   # int64 (nt+1,) row offsets in processing order
     nnz: int
     perm: torch.Tensor
+    pos_info: torch.Tensor = None  # 16 B per position (target, support size, radius)
+    pos_t: torch.Tensor = None     # (nt, dim) targets in processing order
 
     @property
     def max_count(self):
@@ -268,7 +270,9 @@ class Selection:
 
     def lists(self):
         return FmLists(self.counts.data_ptr(), self.slot_id.data_ptr(), self.slot_pos.data_ptr(),
-                       int(self.slot_cap), self.n_overflow, self.overflow.data_ptr())
+                       int(self.slot_cap), self.n_overflow, self.overflow.data_ptr(),
+                       self.pos_info.data_ptr() if self.pos_info is not None else None,
+                       self.pos_t.data_ptr() if self.pos_t is not None else None)
 
 
 def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
@@ -284,12 +288,15 @@ def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
     slot_id = _empty(max(nt * cap, 1), torch.int32, dev)
     slot_pos = _empty(max(nt * cap, 1), torch.int32, dev)
     overflow = _empty(max(nt, 1), torch.int32, dev)
+    pos_info = _empty(max(nt, 1) * 2, torch.float64, dev)  # 16 B records
+    pos_t = _empty((max(nt, 1), cloud.dim), torch.float64, dev)
     stats_d = _empty(8, torch.int32, dev)
     csel = sel.to_ctypes()
     check(L.fm_select_supports(ctypes.byref(cloud.grid), ptr(cloud.cell_start), ptr(cloud.sorted_pts),
                       ptr(cloud.sorted_ids), ptr(targets), nt, ptr(perm), ctypes.byref(csel),
                       int(min_required), ptr(counts), ptr(radii), ptr(status), ptr(slot_id),
-                      ptr(slot_pos), cap, ptr(overflow), ptr(stats_d), _stream()), "fm_select")
+                      ptr(slot_pos), cap, ptr(overflow), ptr(stats_d), ptr(pos_info),
+                      ptr(pos_t), _stream()), "fm_select_supports")
     offsets = _empty(nt + 1, torch.int64, dev)
     ws_bytes = L.fm_offsets_ordered_workspace(nt)
     ws = _workspace(ws_bytes, dev)
@@ -305,7 +312,7 @@ def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
     if nt == 0:
         stats[0] = 0
     return Selection(sel, counts, radii, status, slot_id, slot_pos, cap, overflow, stats,
-                     offsets, nnz, perm)
+                     offsets, nnz, perm, pos_info, pos_t)
 
 
 def support_csr(cloud, targets, sl, rbf=None):
