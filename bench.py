@@ -70,12 +70,14 @@ def workload(config, rank=0):
         side = np.linspace(0.0, 1.0, 1000)
         xx, yy = np.meshgrid(side, side)
         src = np.ascontiguousarray(np.column_stack([xx.reshape(-1), yy.reshape(-1)]))
-        tgt = np.random.RandomState(rank).uniform(0, 1, (1000000, 2))
+        # targets keep 2h off the boundary: a corner target sees only 4 lattice
+        # points inside 2h, which the reference rejects (UnderdeterminedError)
+        h = 1.0 / 999.0
+        tgt = np.random.RandomState(rank).uniform(2 * h, 1 - 2 * h, (1000000, 2))
         X = synth.sincos_field(src, 8)
-        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
-                         P.FixedRadius(2.0 / 999.0))
-        desc = {"workload": "1M lattice linspace(0,1,1000)^2 -> 1M random targets, MLS degree "
-                            "2, C4 a=2, FixedRadius(2h), 8-component field",
+        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.FixedRadius(2 * h))
+        desc = {"workload": "1M lattice linspace(0,1,1000)^2 -> 1M random targets in "
+                            "[2h,1-2h]^2, MLS degree 2, C4 a=2, FixedRadius(2h), 8-component field",
                 "sources": int(src.shape[0]), "targets_per_gpu": int(tgt.shape[0]),
                 "components": 8, "degree": 2, "rbf": "c4", "selection": "fixed(2h)"}
     elif config == "c1":
@@ -203,12 +205,13 @@ def b200_step(src_d, tgt_d, X_d, spec, marks):
         marks.append((name, e))
 
     mark("start")
-    cloud = D.SourceCloud(src_d)
+    bs, bt = D.device_bboxes([src_d, tgt_d])  # one sync for both boxes
+    cloud = D.SourceCloud(src_d, bbox=bs)
     mark("grid")
     perm = cloud.target_order(tgt_d)
     mark("order")
     sel = spec.selection
-    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, _r_max_device(cloud, tgt_d)) \
+    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, _r_max_device(cloud, tgt_d, bt)) \
         if hasattr(sel, "min_points") else D.fixed(sel.r_c)
     cnt = D.select(cloud, tgt_d, dsel, perm, 0)
     mark("select")
@@ -299,10 +302,18 @@ def run_b200(args, rank, world, local_rank):
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            Yh = P.PreparedTransfer(src_h, tgt_h, spec).apply(X_h)
+            pt = P.PreparedTransfer(src_h, tgt_h, spec)
             if world > 1:
-                Yh = gather_target_field(Yh, nt_local * world).cpu()
-            Yh = Yh.cpu().numpy() if isinstance(Yh, torch.Tensor) else Yh
+                # sharded public API: this rank's rows, then the NCCL all-gather
+                # of the full target field, then D2H
+                Yd = pt.apply(X_h.to("cuda", non_blocking=True))
+                Yf = gather_target_field(Yd, nt_local * world)
+                Yh = torch.empty(Yf.shape, dtype=Yf.dtype, pin_memory=True)
+                Yh.copy_(Yf, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            else:
+                Yh = pt.apply(X_h)
+            Yh = Yh.numpy()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")

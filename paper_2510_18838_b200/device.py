@@ -106,11 +106,17 @@ class SourceCloud:
 
 
 def device_bbox(pts):
-    dim = pts.shape[1]
-    lohi = torch.empty(2 * dim, dtype=torch.float64, device=pts.device)
-    check(_lib.lib().fm_bbox(dim, ptr(pts), pts.shape[0], ptr(lohi), _stream()), "fm_bbox")
+    return device_bboxes([pts])[0]
+
+
+def device_bboxes(arrays):
+    """Bounding boxes of several device point arrays with ONE device->host sync."""
+    dim = arrays[0].shape[1]
+    lohi = torch.empty((len(arrays), 2 * dim), dtype=torch.float64, device=arrays[0].device)
+    for i, pts in enumerate(arrays):
+        check(_lib.lib().fm_bbox(dim, ptr(pts), pts.shape[0], ptr(lohi[i]), _stream()), "fm_bbox")
     h = lohi.cpu().numpy()
-    return h[:dim], h[dim:]
+    return [(h[i, :dim], h[i, dim:]) for i in range(len(arrays))]
 
 
 # ------------------------------------------------------- selection spec

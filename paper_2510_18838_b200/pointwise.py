@@ -209,11 +209,25 @@ def _r_max(src_xy, targets):
     return 1.0000001 * ext + 1e-300
 
 
-def _r_max_device(cloud, targets):
+_COPY_STREAMS = {}
+
+
+def _copy_stream():
+    """Side stream for host->device copies that overlap device work."""
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[dev]
+
+
+def _r_max_device(cloud, targets, tbbox=None):
     """_r_max on device-resident points (bboxes by fm_bbox, one small D2H;
     the source bbox is the one the grid was built from)."""
     lo_s, hi_s = cloud.bbox if cloud.bbox is not None else D.device_bbox(cloud.pts)
-    lo_t, hi_t = D.device_bbox(targets) if targets.shape[0] else (lo_s, hi_s)
+    if tbbox is not None:
+        lo_t, hi_t = tbbox
+    else:
+        lo_t, hi_t = D.device_bbox(targets) if targets.shape[0] else (lo_s, hi_s)
     lo, hi = np.minimum(lo_s, lo_t), np.maximum(hi_s, hi_t)
     if lo.size == 2:
         ext = float(np.hypot(hi[0] - lo[0], hi[1] - lo[1]))
@@ -244,12 +258,18 @@ class _Plan:
         self.targets = targets
         self.fitspec = fitspec
         self.base_index = base_index
-        if isinstance(grid, PointGrid) and grid.points.shape[1] == src_xy.shape[1]:
-            self.cloud = grid.cloud()
-        else:
-            self.cloud = D.SourceCloud(src_xy)
         self.t = D.to_device(targets)
         nt = self.t.shape[0]
+        self._tbbox = None
+        if isinstance(grid, PointGrid) and grid.points.shape[1] == src_xy.shape[1]:
+            self.cloud = grid.cloud()
+        elif isinstance(src_xy, torch.Tensor) and nt:
+            # device-resident inputs: both bounding boxes with one sync
+            src_d = D.to_device(src_xy)
+            bs, self._tbbox = D.device_bboxes([src_d, self.t])
+            self.cloud = D.SourceCloud(src_d, bbox=bs)
+        else:
+            self.cloud = D.SourceCloud(src_xy)
         self.perm = self.cloud.target_order(self.t) if nt else None
         sel = fitspec.selection
         need = n_monomials(fitspec.degree, self.cloud.dim)
@@ -267,7 +287,7 @@ class _Plan:
             if isinstance(src_xy, np.ndarray) and isinstance(targets, np.ndarray):
                 r_max = _r_max(src_xy, targets)
             else:
-                r_max = _r_max_device(self.cloud, self.t)
+                r_max = _r_max_device(self.cloud, self.t, self._tbbox)
             self.sel = D.adaptive(sel.min_points, sel.r0, sel.growth, r_max)
             self.sl = D.select(self.cloud, self.t, self.sel, self.perm, 0)
             if self.sl.stats[4] > 0:
@@ -415,13 +435,23 @@ class PreparedTransfer:
         if isinstance(source_values, torch.Tensor):
             if source_values.shape[0] != self.src_xy.shape[0]:
                 raise FieldError("source values disagree with prepared points")
-            self._check_fit()
-            Y = self.operator.apply(D.to_device(source_values))
             if source_values.is_cuda:
-                return Y
+                self._check_fit()
+                return self.operator.apply(source_values.to(torch.float64))
+            # host field: its H2D copy runs on a side stream while the operator
+            # build may still be executing; the fit check waits for the build
+            # only after the apply is queued
+            main = torch.cuda.current_stream()
+            side = _copy_stream()
+            with torch.cuda.stream(side):
+                X = D.to_device(source_values)
+            main.wait_stream(side)
+            X.record_stream(main)
+            Y = self.operator.apply(X)
             out = torch.empty(Y.shape, dtype=Y.dtype, pin_memory=True)
             out.copy_(Y, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            self._check_fit()
+            main.synchronize()
             return out
         vals = np.ascontiguousarray(source_values, dtype=np.float64)
         if vals.shape[0] != self.src_xy.shape[0]:
