@@ -367,6 +367,8 @@ __global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_req
     lb.pos = lb.id + lcap;
     lb.cap = lcap;
     RowTable<G> &rt = *reinterpret_cast<RowTable<G> *>(base + (size_t)lcap * 16);
+    __shared__ RadiusTable tab;
+    fill_radius_table(tab, s.sel);
     const int lane = threadIdx.x & 31, glane = lane & (G - 1);
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -382,37 +384,16 @@ __global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_req
         uint8_t st;
         bool listed;
         const int m = select_target<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, s.sel,
-                                            active, lane, glane, rt, lb, r, st, listed);
+                                            tab, active, lane, glane, rt, lb, r, st, listed);
         if (active) {
             if (listed && m <= slot_cap) {
-                // rank sort by id straight into the slot (ids are distinct)
+                // supports in discovery order (the fit does not need id order;
+                // the reference-format CSR is sorted by fm_support_fill)
                 int32_t *oid = slot_id + k * slot_cap;
                 int32_t *opos = slot_pos + k * slot_cap;
-                // up to 4 entries per lane ranked against pairs of ids (LDS.64)
-                for (int e0 = 0; e0 < m; e0 += 4 * G) {
-                    int32_t myid[4];
-                    int rk[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int e = e0 + u * G + glane;
-                        myid[u] = e < m ? lb.id[e] : INT32_MAX;
-                        rk[u] = 0;
-                    }
-                    for (int f2 = 0; f2 < m; f2 += 2) {
-                        const int2 two = *reinterpret_cast<const int2 *>(lb.id + f2);
-                        const int32_t second = f2 + 1 < m ? two.y : INT32_MAX;
-#pragma unroll
-                        for (int u = 0; u < 4; u++)
-                            rk[u] += (two.x < myid[u]) + (second < myid[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int e = e0 + u * G + glane;
-                        if (e < m) {
-                            oid[rk[u]] = myid[u];
-                            opos[rk[u]] = lb.pos[e];
-                        }
-                    }
+                for (int e = glane; e < m; e += G) {
+                    oid[e] = lb.id[e];
+                    opos[e] = lb.pos[e];
                 }
             } else if (glane == 0) {
                 overflow[atomicAdd(stats + 6, 1)] = (int32_t)k;

@@ -73,13 +73,19 @@ struct Window {
         if (row < nrows) {
             // unravel the row index over axes 1..DIM-1 and measure the squared
             // distance from t to the row's cell box along those axes
-            int64_t rem = row, base = 0;
+            int32_t rem = (int32_t)row;  // window rows fit in 32 bits
+            int64_t base = 0;
             double off2 = 0.0;
 #pragma unroll
             for (int a = 1; a < DIM; a++) {
-                const int64_t span = chi[a] - clo[a] + 1;
-                const int64_t ia = clo[a] + rem % span;
-                rem /= span;
+                int64_t ia;
+                if (a == DIM - 1) {  // last axis: no division needed
+                    ia = clo[a] + rem;
+                } else {
+                    const int32_t span = (int32_t)(chi[a] - clo[a] + 1);
+                    ia = clo[a] + rem % span;
+                    rem /= span;
+                }
                 base += ia * stride[a];
                 const double d = g.d[a];
                 const double blo = ia == 0 ? -INFINITY : g.lo[a] + (double)ia * d;
@@ -281,34 +287,19 @@ __device__ __forceinline__ double sqrt_threshold(double r) {
     return x;
 }
 
-template <int DIM, int G, int NR>
-__device__ __forceinline__ void scan_counts(const GridDev &g, const int32_t *__restrict__ cell_start,
-                                            const double *__restrict__ sorted_pts,
-                                            const int32_t *__restrict__ sorted_ids, const double *t,
-                                            const double (&radii)[NR], int nr, bool active,
-                                            int lane, int glane, RowTable<G> &rt, int (&cnt)[NR],
-                                            ListBuf &lb, int &nlist) {
-    double rscan = 0.0;  // radii[nr - 1], selected statically (keeps radii in registers)
-#pragma unroll
-    for (int j = 0; j < NR; j++)
-        if (active && j == nr - 1) rscan = radii[j];
-    // thresholds of radii[0..nr-1]: one lane each, then broadcast to the group
-    static_assert(NR <= G, "one lane per radius");
-    double my_r = 0.0;
-#pragma unroll
-    for (int j = 0; j < NR; j++)
-        if (glane == j) my_r = radii[j];
-    const double my_thr = (active && glane < nr) ? sqrt_threshold(my_r) : 0.0;
-    const int gbase = lane & ~(G - 1);
-    double thr[NR];
-    double thr_scan = 0.0;
-    static_for<0, NR>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        thr[j] = __shfl_sync(FM_FULL_MASK, my_thr, gbase + j);
-        if (j == nr - 1) thr_scan = thr[j];
-    });
+// One window scan at radius r (threshold thr = sqrt_threshold(r)): returns
+// #{d < r} and appends every candidate with d < r (id, grid position, d^2)
+// to the group's list (entries beyond cap are counted, not stored).
+// Warp-collective.
+template <int DIM, int G>
+__device__ __forceinline__ int scan_list(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                         const double *__restrict__ sorted_pts,
+                                         const int32_t *__restrict__ sorted_ids, const double *t,
+                                         double r, double thr, bool active, int lane, int glane,
+                                         RowTable<G> &rt, ListBuf &lb, int &nlist) {
     const unsigned lt_mask = (1u << glane) - 1u;
-    Window<DIM, G> w(g, t, rscan, active);
+    int cnt = 0;
+    Window<DIM, G> w(g, t, r, active);
     for (int ch = 0; ch < w.nchunks_w; ch++) {
         const int iters = w.chunk(g, cell_start, t, ch, glane, rt);
         for (int it = 0; it < iters; it++) {
@@ -322,7 +313,7 @@ __device__ __forceinline__ void scan_counts(const GridDev &g, const int32_t *__r
                 load_point<DIM>(sorted_pts, pos, p);
                 d2 = dist2_rn<DIM>(p, t);
             }
-            const bool keep = d2 < thr_scan;
+            const bool keep = d2 < thr;
             const unsigned bits = group_bits<G>(__ballot_sync(FM_FULL_MASK, keep), lane);
             if (keep) {
                 const int o = nlist + __popc(bits & lt_mask);
@@ -333,15 +324,55 @@ __device__ __forceinline__ void scan_counts(const GridDev &g, const int32_t *__r
                 }
             }
             nlist += __popc(bits);
-            static_for<0, NR>([&](auto jc) {
-                constexpr int j = decltype(jc)::value;
-                cnt[j] += __popc(group_bits<G>(__ballot_sync(FM_FULL_MASK, j < nr && d2 < thr[j]),
-                                               lane));
-            });
+            cnt += __popc(bits);
         }
         __syncwarp();
     }
-    __syncwarp();
+    return cnt;
+}
+
+// The reference's radius sequence r_0 = r0, r_{j+1} = min(r_j * growth, r_max)
+// (_ext.pyx:258-270) -- the same for every target -- with the exact
+// thresholds T(r_j), tabulated once per CTA.  Fixed radius: entry 0 = r_c.
+constexpr int kRadTab = 64;
+struct RadiusTable {
+    double r[kRadTab];
+    double thr[kRadTab];
+};
+
+__device__ __forceinline__ void fill_radius_table(RadiusTable &tab, const fm_select &sel) {
+    const int j = threadIdx.x;
+    if (j < kRadTab) {
+        double r;
+        if (sel.adaptive) {
+            r = sel.r0;
+            for (int i = 0; i < j && r < sel.r_max; i++) {
+                r = r * sel.growth;
+                if (r > sel.r_max) r = sel.r_max;
+            }
+        } else {
+            r = sel.r_c;
+        }
+        tab.r[j] = r;
+        tab.thr[j] = sqrt_threshold(r);
+    }
+    __syncthreads();
+}
+
+// radius j of the sequence (beyond the table: continued on the fly)
+__device__ __forceinline__ void seq_radius(const RadiusTable &tab, const fm_select &sel, int j,
+                                           double &r, double &thr) {
+    if (j < kRadTab) {
+        r = tab.r[j];
+        thr = tab.thr[j];
+        return;
+    }
+    r = tab.r[kRadTab - 1];
+    for (int i = kRadTab - 1; i < j && r < sel.r_max; i++) {
+        r = r * sel.growth;
+        if (r > sel.r_max) r = sel.r_max;
+    }
+    thr = sqrt_threshold(r);
 }
 
 // Density guess of the number of growth steps (2-D): sources in the 3x3
@@ -407,32 +438,24 @@ template <int DIM, int G>
 __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__restrict__ cell_start,
                                              const double *__restrict__ sorted_pts,
                                              const int32_t *__restrict__ sorted_ids,
-                                             const double *t, const fm_select &sel, bool active,
-                                             int lane, int glane, RowTable<G> &rt, ListBuf &lb,
+                                             const double *t, const fm_select &sel,
+                                             const RadiusTable &tab, bool active, int lane,
+                                             int glane, RowTable<G> &rt, ListBuf &lb,
                                              double &r_out, uint8_t &status, bool &listed) {
-    // radius of the first scan: r_kg of the reference sequence (or r_c)
-    double rscan = sel.r_c;
+    // first scan at step kg of the sequence (stopping at r_max)
     int kg = 0;
     if (sel.adaptive) {
         kg = guess_steps<DIM, G>(g, cell_start, t, sel, active, glane);
-        double r = sel.r0;
         int j = 0;
-        while (j < kg && r < sel.r_max) {
-            r = r * sel.growth;
-            if (r > sel.r_max) r = sel.r_max;
-            j++;
-        }
+        while (j < kg && tab.r[j < kRadTab ? j : kRadTab - 1] < sel.r_max && j + 1 < kRadTab) j++;
         kg = j;
-        rscan = r;
     }
-    int m = 0, nlist = 0;
-    {
-        double r1[1] = {active ? rscan : 0.0};
-        int c1[1] = {0};
-        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, active, lane,
-                               glane, rt, c1, lb, nlist);
-        m = c1[0];
-    }
+    double rscan, thr_scan;
+    seq_radius(tab, sel, kg, rscan, thr_scan);
+    int nlist = 0;
+    int m = scan_list<DIM, G>(g, cell_start, sorted_pts, sorted_ids, t, rscan, thr_scan, active,
+                              lane, glane, rt, lb, nlist);
+    int jf = kg;  // index of the final radius in the sequence
     double rf = rscan;
     status = 0;
     bool done = !active || !sel.adaptive;
@@ -447,51 +470,43 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
         }
     }
     // smaller radii of the sequence, counted on the list (kg is small)
-    const int kg_w = warp_max_int(active && sel.adaptive && !slow && m >= sel.min_pts ? kg : 0);
+    const bool recount = active && sel.adaptive && !slow && m >= sel.min_pts && kg > 0;
+    const int kg_w = warp_max_int(recount ? kg : 0);
     {
-        double r = sel.r0;
-        bool found = !(active && sel.adaptive && !slow && m >= sel.min_pts && kg > 0);
+        bool found = !recount;
         for (int j = 0; j < kg_w; j++) {
             const bool mine = !found && j < kg;
-            const double thr = mine ? sqrt_threshold(r) : 0.0;
+            const double thr = mine ? tab.thr[j] : 0.0;
             const int c = count_list<G>(lb, mine ? nlist : 0, thr, lane, glane);
             if (mine && c >= sel.min_pts) {
                 found = true;
                 m = c;
-                rf = r;
-            }
-            if (mine) {
-                r = r * sel.growth;
-                if (r > sel.r_max) r = sel.r_max;
+                jf = j;
+                rf = tab.r[j];
             }
         }
     }
     if (slow) {  // rare: recount from r0 one scan per radius
-        rf = sel.r0;
+        jf = -1;
         done = false;
     }
     // continue the sequence one radius at a time (_ext.pyx:259-270)
     bool fresh = false;  // list rebuilt at exactly rf
-    bool first = true;
     while (__any_sync(FM_FULL_MASK, !done)) {
-        double r1[1] = {0.0};
-        int c1[1] = {0};
         const bool go = !done;
+        double r1 = 0.0, thr1 = 0.0;
         if (go) {
-            if (!(slow && first)) {
-                rf = rf * sel.growth;
-                if (rf > sel.r_max) rf = sel.r_max;
-            }
-            r1[0] = rf;
+            jf++;
+            seq_radius(tab, sel, jf, r1, thr1);
+            rf = r1;
             nlist = 0;
         }
-        first = false;
         int nl = nlist;
-        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, go, lane, glane,
-                               rt, c1, lb, nl);
+        const int c = scan_list<DIM, G>(g, cell_start, sorted_pts, sorted_ids, t, r1, thr1, go,
+                                        lane, glane, rt, lb, nl);
         if (go) {
             nlist = nl;
-            m = c1[0];
+            m = c;
             fresh = true;
             if (m >= sel.min_pts) {
                 done = true;
@@ -503,20 +518,22 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
     }
     // keep only d < rf when the list came from the wider first scan; rescan
     // when that scan overflowed the buffer but the final support fits
-    const bool wide = active && !fresh && rf < rscan;
+    const bool wide = active && !fresh && jf < kg;
     const bool rescan = wide && nlist > lb.cap && m <= lb.cap;
+    double rthr = 0.0;
+    if (wide) {
+        double rr;
+        seq_radius(tab, sel, jf, rr, rthr);
+    }
     if (__any_sync(FM_FULL_MASK, rescan)) {
-        double r1[1] = {rescan ? rf : 0.0};
-        int c1[1] = {0};
         int nl = 0;
-        scan_counts<DIM, G, 1>(g, cell_start, sorted_pts, sorted_ids, t, r1, 1, rescan, lane,
-                               glane, rt, c1, lb, nl);
+        scan_list<DIM, G>(g, cell_start, sorted_pts, sorted_ids, t, rescan ? rf : 0.0,
+                          rescan ? rthr : 0.0, rescan, lane, glane, rt, lb, nl);
         if (rescan) nlist = nl;
     }
     const bool filter = wide && !rescan && nlist <= lb.cap;
     const int nf = filter ? nlist : 0;
     const int iters = warp_max_int((nf + G - 1) / G);
-    const double thr_f = filter ? sqrt_threshold(rf) : 0.0;
     int kept = 0;
     const unsigned lt_mask = (1u << glane) - 1u;
     for (int it = 0; it < iters; it++) {
@@ -529,7 +546,7 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
             pos = lb.pos[e];
             d = lb.d[e];
         }
-        const bool keep = in && d < thr_f;
+        const bool keep = in && d < rthr;
         const unsigned bits = group_bits<G>(__ballot_sync(FM_FULL_MASK, keep), lane);
         if (keep) {
             const int o = kept + __popc(bits & lt_mask);
