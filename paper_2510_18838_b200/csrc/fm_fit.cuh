@@ -146,11 +146,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         }
     }
 
-    // row slots holding a support or ridge row anywhere in the warp (a prefix);
-    // the others are all-zero everywhere and are skipped by warp-uniform branches
-    const int rows_used = m + (ridge ? K : 0);
-    const int nql = warp_max_int((rows_used + G - 1) / G);
-
     // ---- Householder QR, column by column
     double gam[K], beta[K], inv_beta[K], v0[K];
     static_for<0, K>([&](auto jc) {
@@ -159,7 +154,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         double sl = 0.0;
 #pragma unroll
         for (int q = 0; q < ROWS; q++) {
-                if (q > 0 && q >= nql) continue;  // slot dead in the whole warp
             const int i = q * G + glane;
             if (row_below<G>(q, j, glane)) sl = fma(A[q][j], A[q][j], sl);
             (void)i;
@@ -190,7 +184,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double pl = 0.0;
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
-                if (q > 0 && q >= nql) continue;  // slot dead in the whole warp
                 const int i = q * G + glane;
                 if (row_diag<G>(q, j, glane)) pl = fma(vj, A[q][l], pl);
                 else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], A[q][l], pl);
@@ -205,7 +198,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             const double td = gj * dot[l];
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
-                if (q > 0 && q >= nql) continue;  // slot dead in the whole warp
                 const int i = q * G + glane;
                 if (row_diag<G>(q, j, glane)) A[q][l] = fma(-td, vj, A[q][l]);
                 else if (row_below<G>(q, j, glane)) A[q][l] = fma(-td, A[q][j], A[q][l]);
@@ -310,7 +302,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double pl = 0.0;
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
-                if (q > 0 && q >= nql) continue;  // slot dead in the whole warp
                 const int i = q * G + glane;
                 if (row_diag<G>(q, j, glane)) pl = fma(v0[j], yy[q], pl);
                 else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], yy[q], pl);
@@ -319,7 +310,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             const double td = gam[j] * group_sum<G>(pl);
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
-                if (q > 0 && q >= nql) continue;  // slot dead in the whole warp
                 const int i = q * G + glane;
                 if (row_diag<G>(q, j, glane)) yy[q] = fma(-td, v0[j], yy[q]);
                 else if (row_below<G>(q, j, glane)) yy[q] = fma(-td, A[q][j], yy[q]);
