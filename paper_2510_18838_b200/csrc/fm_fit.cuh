@@ -222,25 +222,51 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     }
     __syncwarp();
 
-    // ---- rank test: kappa_1(R) = ||R||_1 ||R^-1||_1 (lane l owns column l)
-    double colsum = 0.0, invsum = 0.0;
-    {
-        const int l = glane;
-        double x[K];
+    // ---- rank test: kappa_1(R) = ||R||_1 ||R^-1||_1 >= 1.5/eps (lam = 0 only).
+    // A cheap upper bound first -- with delta = min|r_ii|, M = max|r_ij| (i<j),
+    // D = max|r_ii|: kappa_1 <= K max(M, D) (1 + M/delta)^(K-1) / delta -- and
+    // the exact kappa only for warps where the bound cannot rule it out.
+    bool singular = false;
+    if (!ridge) {
+        double offmax = 0.0, dmin = INFINITY, dmax = 0.0;
+        if (glane < K) {
+            const int l = glane;
+            const double d = fabs(sR[l * K + l]);
+            dmin = d;
+            dmax = d;
 #pragma unroll
-        for (int i = K - 1; i >= 0; i--) {
-            double acc = (i == l) ? 1.0 : 0.0;
+            for (int c = 1; c < K; c++)
+                if (c > l) offmax = fmax(offmax, fabs(sR[l * K + c]));
+        }
+        offmax = group_max<G>(offmax);
+        dmax = group_max<G>(dmax);
+        dmin = -group_max<G>(-dmin);
+        double growth = 1.0;
+        const double ratio = 1.0 + offmax / dmin;
 #pragma unroll
-            for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
-            x[i] = (i <= l) ? acc * inv_beta[i] : 0.0;
-            if (i <= l && l < K) {
-                colsum += fabs(sR[i * K + l]);
-                invsum += fabs(x[i]);
+        for (int i = 1; i < K; i++) growth *= ratio;
+        const double bound = (double)K * fmax(offmax, dmax) * growth / dmin;
+        const bool unsure = !(bound < 1e12);  // NaN / inf / large: decide exactly
+        if (__any_sync(FM_FULL_MASK, unsure)) {
+            double colsum = 0.0, invsum = 0.0;
+            const int l = glane;
+            double x[K];
+#pragma unroll
+            for (int ii = 0; ii < K; ii++) {
+                const int i = K - 1 - ii;
+                double acc = (i == l) ? 1.0 : 0.0;
+#pragma unroll
+                for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
+                x[i] = (i <= l) ? acc * inv_beta[i] : 0.0;
+                if (i <= l && l < K) {
+                    colsum += fabs(sR[i * K + l]);
+                    invsum += fabs(x[i]);
+                }
             }
+            const double kappa = group_max<G>(colsum) * group_max<G>(invsum);
+            singular = unsure && !(kappa < kSingularKappa);
         }
     }
-    const double kappa = group_max<G>(colsum) * group_max<G>(invsum);
-    const bool singular = !ridge && !(kappa < kSingularKappa);
     const int status = empty ? FM_FIT_EMPTY : (singular ? FM_FIT_SINGULAR : FM_FIT_OK);
 
     if (SOLVE) {
