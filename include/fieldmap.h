@@ -185,9 +185,10 @@ int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int6
                 int32_t *stats, fm_stream_t stream);
 
 /* ----------------------------- a3/a4 + lists: the select pass (new)
- * Count pass that also emits every target's support, sorted by source id
- * (the order of _sort_by_id, _ext.pyx:155-169), into a fixed-stride slot
- * buffer indexed by PROCESSING POSITION k (the k-th entry of perm):
+ * Count pass that also emits every target's support (the reference's set,
+ * in discovery order; fm_support_fill gives the id-sorted CSR of
+ * _sort_by_id, _ext.pyx:155-169) into a fixed-stride slot buffer indexed by
+ * PROCESSING POSITION k (the k-th entry of perm):
  * slot_id/slot_pos[k*slot_cap + i] = source id / index into sorted_pts.
  * counts/radii/status are indexed by target and equal fm_support_count's.
  * Adaptive selection evaluates several radii of the reference's growth
@@ -207,13 +208,25 @@ int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const dou
                        void *pos_info, double *pos_targets, fm_stream_t stream);
 
 /* Row offsets of an operator stored in processing order:
- * offsets[k+1] = offsets[k] + counts[perm[k]] (perm may be NULL). */
+ * offsets[k+1] = offsets[k] + counts[perm[k]] (perm may be NULL).
+ * Optionally (bucket_list != NULL) also partitions the positions by support
+ * size for the build: position k with counts[perm[k]] <= slot_cap goes to
+ * bucket b = the first with size <= FM_BUCKET_EDGES[b], at
+ * bucket_list[b * n + i] (order within a bucket unspecified), and
+ * bucket_count (device int32[FM_NBUCKETS], written by the call) holds the
+ * bucket sizes.  The build then runs one fit shape (lanes x rows per lane)
+ * per bucket instead of sizing every fit for the largest support. */
+#define FM_NBUCKETS 9
+#define FM_BUCKET_EDGES {8, 16, 24, 32, 48, 64, 96, 128, 2147483647}
 size_t fm_offsets_ordered_workspace(int64_t n);
-int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int64_t *offsets,
+int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int32_t slot_cap,
+                       int64_t *offsets, int32_t *bucket_list, int32_t *bucket_count,
                        void *workspace, size_t workspace_bytes, fm_stream_t stream);
 
 /* Supports produced by fm_select (device pointers; n_overflow is the host
- * copy of stats[6]). */
+ * copy of stats[6]).  With bucket_list (fm_offsets_ordered's, stride
+ * bucket_stride = nt, bucket_count = host copy of its counts) the build
+ * launches once per non-empty bucket; without it once over every position. */
 typedef struct fm_lists {
     const int32_t *counts;
     const int32_t *slot_id;
@@ -223,6 +236,9 @@ typedef struct fm_lists {
     const int32_t *overflow;
     const void *pos_info;       /* optional, from fm_select_supports */
     const double *pos_targets;  /* optional, from fm_select_supports */
+    const int32_t *bucket_list; /* optional, from fm_offsets_ordered */
+    int64_t bucket_stride;
+    int32_t bucket_count[FM_NBUCKETS];
 } fm_lists;
 
 /* --------------------------------- a8/a13: transfer operator (new)

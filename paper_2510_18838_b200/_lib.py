@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libfieldmap.so")
+LIB_PATH = os.environ.get("FM_LIB_PATH") or os.path.join(_PKG, "_lib", "libfieldmap.so")
 
 FM_OK = 0
 FM_ERR_ARG = -1
@@ -18,6 +18,8 @@ FM_ERR_CUDA = -2
 FM_ERR_UNSUPPORTED = -3
 FM_ERR_WORKSPACE = -4
 FM_MAX_DIM = 5
+FM_NBUCKETS = 9
+FM_BUCKET_EDGES = (8, 16, 24, 32, 48, 64, 96, 128, 2147483647)
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -48,7 +50,8 @@ class FmFit(ctypes.Structure):
 class FmLists(ctypes.Structure):
     _fields_ = [("counts", c_vp), ("slot_id", c_vp), ("slot_pos", c_vp), ("slot_cap", c_i32),
                 ("n_overflow", c_i32), ("overflow", c_vp), ("pos_info", c_vp),
-                ("pos_targets", c_vp)]
+                ("pos_targets", c_vp), ("bucket_list", c_vp), ("bucket_stride", c_i64),
+                ("bucket_count", c_i32 * FM_NBUCKETS)]
 
 
 P = ctypes.POINTER
@@ -75,7 +78,8 @@ SIGNATURES = {
                                    c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                                    c_vp, c_vp]),
     "fm_offsets_ordered_workspace": (c_sz, [c_i64]),
-    "fm_offsets_ordered": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "fm_offsets_ordered": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                   c_vp]),
     "fm_build_operator": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
                                   c_vp, P(FmLists), c_vp, c_i32, P(FmRbf), P(FmFit), c_vp, c_vp,
                                   c_vp, c_vp, c_vp]),

@@ -313,7 +313,8 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
     if (fit->dim != grid->dim || rbf->kind < 0 || rbf->kind > 7) return FM_ERR_ARG;
     if (sel->adaptive && !radii) return FM_ERR_ARG;
     if (lists && (!lists->counts || !lists->slot_id || !lists->slot_pos || lists->slot_cap < 1 ||
-                  lists->n_overflow < 0 || (lists->n_overflow > 0 && !lists->overflow)))
+                  lists->n_overflow < 0 || (lists->n_overflow > 0 && !lists->overflow) ||
+                  (lists->bucket_list && lists->bucket_stride < nt)))
         return FM_ERR_ARG;
     const SearchArgs s = make_search(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm,
                                      sel, sel->adaptive ? radii : nullptr);
@@ -341,8 +342,24 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
         b.pos_info = reinterpret_cast<const PosInfo *>(lists->pos_info);
         b.pos_t = lists->pos_targets;
         const int mm = max_count < lists->slot_cap ? max_count : lists->slot_cap;
-        rc = dispatch_build(grid->dim, fit->degree, solve, true, s, b, mm, st);
-        if (rc || lists->n_overflow == 0) return rc;
+        if (lists->bucket_list) {
+            // one launch per non-empty size bucket, each with the fit shape
+            // (lanes x rows per lane) of the bucket's largest support
+            constexpr int edges[FM_NBUCKETS] = FM_BUCKET_EDGES;
+            for (int bk = 0; bk < FM_NBUCKETS; bk++) {
+                if (lists->bucket_count[bk] <= 0) continue;
+                BuildArgs bb = b;
+                bb.klist = lists->bucket_list + (int64_t)bk * lists->bucket_stride;
+                bb.nk = lists->bucket_count[bk];
+                rc = dispatch_build(grid->dim, fit->degree, solve, true, s, bb,
+                                    edges[bk] < mm ? edges[bk] : mm, st);
+                if (rc) return rc;
+            }
+        } else {
+            rc = dispatch_build(grid->dim, fit->degree, solve, true, s, b, mm, st);
+            if (rc) return rc;
+        }
+        if (lists->n_overflow == 0) return FM_OK;
         b.klist = lists->overflow;
         b.nk = lists->n_overflow;
     }
@@ -401,17 +418,22 @@ size_t fm_offsets_ordered_workspace(int64_t n) {
     return align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)) + scan_workspace_bytes(n);
 }
 
-int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int64_t *offsets,
+int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int32_t slot_cap,
+                       int64_t *offsets, int32_t *bucket_list, int32_t *bucket_count,
                        void *workspace, size_t workspace_bytes, fm_stream_t stream) {
-    if (n < 0) return FM_ERR_ARG;
+    if (n < 0 || (bucket_list && !bucket_count)) return FM_ERR_ARG;
     if (workspace_bytes < fm_offsets_ordered_workspace(n)) return FM_ERR_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *tmp = reinterpret_cast<int32_t *>(workspace);
     char *scan_ws = reinterpret_cast<char *>(workspace) +
                     align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    if (bucket_list &&
+        cudaMemsetAsync(bucket_count, 0, sizeof(int32_t) * FM_NBUCKETS, st) != cudaSuccess)
+        return FM_ERR_CUDA;
     if (n > 0) {
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
-        k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, tmp);
+        k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, tmp, slot_cap, bucket_list,
+                                                bucket_count);
         FM_CHECK_LAUNCH();
     }
     return exclusive_scan<int32_t, int64_t>(tmp, n, offsets, scan_ws, scan_workspace_bytes(n), st);

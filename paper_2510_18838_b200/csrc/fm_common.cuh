@@ -280,9 +280,12 @@ __device__ __forceinline__ int group_scan_incl(int v, int glane) {
 }
 template <int G>
 __device__ __forceinline__ unsigned group_bits(unsigned ballot, int lane) {
-    if (G == 32) return ballot;
-    const int base = lane & ~(G - 1);
-    return (ballot >> base) & ((1u << G) - 1u);
+    if constexpr (G == 32) {
+        return ballot;
+    } else {
+        const int base = lane & ~(G - 1);
+        return (ballot >> base) & ((1u << G) - 1u);
+    }
 }
 
 __device__ __forceinline__ int warp_max_int(int v) { return __reduce_max_sync(FM_FULL_MASK, v); }

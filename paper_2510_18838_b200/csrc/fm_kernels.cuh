@@ -238,7 +238,15 @@ struct BuildArgs {
 };
 
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
-__global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 4) ? 4 : 1) k_build(SearchArgs s,
+#ifndef FM_BUILD_MINB8
+#define FM_BUILD_MINB8 4
+#endif
+#ifndef FM_BUILD_MINB8_R2
+#define FM_BUILD_MINB8_R2 4
+#endif
+__global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MINB8_R2
+                                          : (G == 8 && ROWS <= 4) ? FM_BUILD_MINB8
+                                                                  : 1) k_build(SearchArgs s,
                                                                                  BuildArgs b) {
     constexpr int K = Monos<DIM, DEG>::K;
     extern __shared__ __align__(16) char smem[];
@@ -435,13 +443,43 @@ __global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_req
     warp_flush_pair(stats + 4, nstat, first_stat);
 }
 
-// counts in processing order (input of the ordered offsets scan)
+// size bucket of a support (fieldmap.h FM_BUCKET_EDGES)
+__device__ __forceinline__ int bucket_of(int m) {
+    constexpr int edges[FM_NBUCKETS] = FM_BUCKET_EDGES;
+    int b = 0;
+#pragma unroll
+    for (int i = 0; i < FM_NBUCKETS - 1; i++) b += m > edges[i];
+    return b;
+}
+
+// counts in processing order (input of the ordered offsets scan) and,
+// with bucket_list, the positions partitioned by support size
+// (warp-aggregated appends: one atomic per bucket present in a warp)
 static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
                                 const int32_t *__restrict__ perm, int64_t n,
-                                int32_t *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = counts[perm ? perm[i] : i];
+                                int32_t *__restrict__ out, int slot_cap,
+                                int32_t *__restrict__ bucket_list,
+                                int32_t *__restrict__ bucket_count) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+         base += stride) {
+        const int64_t i = base + lane;
+        const int m = i < n ? counts[perm ? perm[i] : i] : 0;
+        if (i < n) out[i] = m;
+        if (bucket_list) {
+            const int b = (i < n && m <= slot_cap) ? bucket_of(m) : -1;
+            const unsigned peers = __match_any_sync(FM_FULL_MASK, b);
+            if (b >= 0) {
+                const int leader = __ffs(peers) - 1;
+                int at = 0;
+                if (lane == leader) at = atomicAdd(bucket_count + b, __popc(peers));
+                at = __shfl_sync(peers, at, leader);
+                bucket_list[(int64_t)b * n + at + __popc(peers & ((1u << lane) - 1u))] =
+                    (int32_t)i;
+            }
+        }
+    }
 }
 
 // ------------------------------------------------- fit_many (CSR input)
@@ -605,6 +643,7 @@ int launch_build(const SearchArgs &s, const BuildArgs &b, int max_m, cudaStream_
 #define FM_BUILD(GG, R) launch_build_rows<DIM, DEG, GG, R, SOLVE, FROM_SLOTS>(s, b, st)
     if (need <= G0) return FM_BUILD(G0, 1);
     if (need <= 2 * G0) return FM_BUILD(G0, 2);
+    if (need <= 3 * G0) return FM_BUILD(G0, 3);
     if (need <= 4 * G0) return FM_BUILD(G0, 4);
     if constexpr (G0 < 32) {
         if (need <= 128) return FM_BUILD(32, 4);

@@ -265,6 +265,8 @@ class Selection:
     perm: torch.Tensor
     pos_info: torch.Tensor = None  # 16 B per position (target, support size, radius)
     pos_t: torch.Tensor = None     # (nt, dim) targets in processing order
+    bucket_list: torch.Tensor = None  # int32 (FM_NBUCKETS * nt) positions by support size
+    bucket_count: np.ndarray = None   # int32[FM_NBUCKETS] host
 
     @property
     def max_count(self):
@@ -275,10 +277,15 @@ class Selection:
         return int(self.stats[6])
 
     def lists(self):
+        nb = _lib.FM_NBUCKETS
+        buckets = self.bucket_list is not None and self.bucket_count is not None
         return FmLists(self.counts.data_ptr(), self.slot_id.data_ptr(), self.slot_pos.data_ptr(),
                        int(self.slot_cap), self.n_overflow, self.overflow.data_ptr(),
                        self.pos_info.data_ptr() if self.pos_info is not None else None,
-                       self.pos_t.data_ptr() if self.pos_t is not None else None)
+                       self.pos_t.data_ptr() if self.pos_t is not None else None,
+                       self.bucket_list.data_ptr() if buckets else None,
+                       self.counts.shape[0] if buckets else 0,
+                       (ctypes.c_int32 * nb)(*(self.bucket_count if buckets else [0] * nb)))
 
 
 def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
@@ -296,7 +303,9 @@ def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
     overflow = _empty(max(nt, 1), torch.int32, dev)
     pos_info = _empty(max(nt, 1) * 2, torch.float64, dev)  # 16 B records
     pos_t = _empty((max(nt, 1), cloud.dim), torch.float64, dev)
-    stats_d = _empty(8, torch.int32, dev)
+    nb = _lib.FM_NBUCKETS
+    stats_d = _empty(8 + nb, torch.int32, dev)  # select stats + bucket sizes
+    blist = _empty(max(nt, 1) * nb, torch.int32, dev)
     csel = sel.to_ctypes()
     check(L.fm_select_supports(ctypes.byref(cloud.grid), ptr(cloud.cell_start), ptr(cloud.sorted_pts),
                       ptr(cloud.sorted_ids), ptr(targets), nt, ptr(perm), ctypes.byref(csel),
@@ -306,19 +315,20 @@ def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
     offsets = _empty(nt + 1, torch.int64, dev)
     ws_bytes = L.fm_offsets_ordered_workspace(nt)
     ws = _workspace(ws_bytes, dev)
-    check(L.fm_offsets_ordered(ptr(counts), ptr(perm), nt, ptr(offsets), ptr(ws), ws_bytes,
-                               _stream()), "fm_offsets_ordered")
-    host = torch.empty(10, dtype=torch.int32, pin_memory=True)
-    host[:8].copy_(stats_d, non_blocking=True)
-    host[8:10].copy_(offsets[nt:nt + 1].view(torch.int32), non_blocking=True)
+    check(L.fm_offsets_ordered(ptr(counts), ptr(perm), nt, cap, ptr(offsets), ptr(blist),
+                               ptr(stats_d[8:]), ptr(ws), ws_bytes, _stream()),
+          "fm_offsets_ordered")
+    host = torch.empty(8 + nb + 2, dtype=torch.int32, pin_memory=True)
+    host[:8 + nb].copy_(stats_d, non_blocking=True)
+    host[8 + nb:].copy_(offsets[nt:nt + 1].view(torch.int32), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     h = host.numpy()
     stats = h[:8].copy()
-    nnz = int(h[8:10].view(np.int64)[0])
+    nnz = int(h[8 + nb:].view(np.int64)[0])
     if nt == 0:
         stats[0] = 0
     return Selection(sel, counts, radii, status, slot_id, slot_pos, cap, overflow, stats,
-                     offsets, nnz, perm, pos_info, pos_t)
+                     offsets, nnz, perm, pos_info, pos_t, blist, h[8:8 + nb].copy())
 
 
 def support_csr(cloud, targets, sl, rbf=None):
