@@ -256,10 +256,16 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
     const int lane = threadIdx.x & 31, glane = lane & (G - 1);
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    // the next tile's klist entry is loaded one iteration ahead
+    int32_t k_next = (b.klist && warp * GPW + lane / G < b.nk) ? b.klist[warp * GPW + lane / G] : 0;
     for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
         const int64_t ii = tile * GPW + lane / G;
         bool active = ii < b.nk;
-        const int64_t k = active ? (b.klist ? (int64_t)b.klist[ii] : ii) : 0;
+        const int64_t k = active ? (b.klist ? (int64_t)k_next : ii) : 0;
+        if (b.klist) {
+            const int64_t iin = ii + nwarps * GPW;
+            k_next = iin < b.nk ? b.klist[iin] : 0;
+        }
         int64_t tid;
         double t[DIM];
         double r;
@@ -290,13 +296,27 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
         }
         bool valid[ROWS];
         double p[ROWS][DIM], w[ROWS], f[ROWS];
-        int32_t ids[ROWS];
+        int32_t ids[ROWS], spos[ROWS];
+        if (FROM_SLOTS) {
+            // slot loads do not wait for m (in-bounds garbage past it is never
+            // used), so they overlap the position-record loads
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+                ids[q] = 0;
+                spos[q] = 0;
+                if (i < b.slot_cap) {
+                    ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
+                    spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
+                }
+            }
+        }
         const double inv_r = active ? 1.0 / r : 0.0;
 #pragma unroll
         for (int q = 0; q < ROWS; q++) {
             const int i = q * G + glane;
             valid[q] = i < m;
-            ids[q] = 0;
+            if (!FROM_SLOTS) ids[q] = 0;
             w[q] = 0.0;
             f[q] = 0.0;
 #pragma unroll
@@ -304,8 +324,7 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
             if (valid[q]) {
                 int32_t pos;
                 if (FROM_SLOTS) {
-                    ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
-                    pos = __ldg(b.slot_pos + k * b.slot_cap + i);
+                    pos = spos[q];
                 } else {
                     ids[q] = gs.sid[i];
                     pos = gs.spos[i];

@@ -5,4 +5,4 @@ CONFIG=${3:-c2}
 mkdir -p gpurun_out
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --config $CONFIG"
 timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$REGEX" -c 3 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncufull=$? >> gpurun_out/status_$TAG.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$REGEX" -c ${4:-3} -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncufull=$? >> gpurun_out/status_$TAG.txt
