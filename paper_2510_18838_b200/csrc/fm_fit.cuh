@@ -54,7 +54,9 @@ struct FitShape {
 // Returns the group-uniform status (FM_FIT_*).
 // Inputs per lane/row q (row index i = q*G + glane): valid[q] (i < m),
 // p[q] source coordinates, w[q] weight (already |w|), f[q] field value
-// (SOLVE only).  sR: K*K doubles, sQ: K doubles of per-group shared memory.
+// (SOLVE only).  sR: K*K doubles, sQ: 4K doubles of per-group shared memory
+// (Q^T b, then gamma, 1/beta and v_0 of every reflector: lane-uniform values
+// kept out of registers between the factorisation and the back-substitution).
 // OP: y[q] receives the operator weight of row i (0 for invalid rows).
 // SOLVE: coeffs[K] (lane-uniform) and value.
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
@@ -102,13 +104,14 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     double s = __dsqrt_rn(group_max<G>(smax_l));
     if (s == 0.0) s = 1.0;
     const double inv_s = 1.0 / s;
-    double spow[K];
-#pragma unroll
-    for (int c = 0; c < K; c++)
-        spow[c] = M.deg[c] == 0 ? 1.0
-                  : M.deg[c] == 1 ? s
-                  : M.deg[c] == 2 ? mul_rn(s, s)
-                                  : mul_rn(mul_rn(s, s), s);
+    // s^deg(c), recomputed where needed rather than held in registers
+    auto spow = [&](int c) {
+        return M.deg[c] == 0 ? 1.0
+               : M.deg[c] == 1 ? s
+               : M.deg[c] == 2 ? mul_rn(s, s)
+                               : mul_rn(mul_rn(s, s), s);
+    };
+    double *sGam = sQ + K, *sIb = sQ + 2 * K, *sV0 = sQ + 3 * K;
 
     // ---- weighted scaled Vandermonde rows (_ext.pyx:374-394)
     double A[ROWS][NC];
@@ -136,7 +139,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         const double sl = sqrt(fp.lam);
         double rdiag[K];
 #pragma unroll
-        for (int c = 0; c < K; c++) rdiag[c] = __ddiv_rn(sl, spow[c]);
+        for (int c = 0; c < K; c++) rdiag[c] = __ddiv_rn(sl, spow(c));
 #pragma unroll
         for (int q = 0; q < ROWS; q++) {
             const int col = q * G + glane - m;
@@ -147,7 +150,6 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     }
 
     // ---- Householder QR, column by column
-    double gam[K], beta[K], inv_beta[K], v0[K];
     static_for<0, K>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         const double x0 = __shfl_sync(FM_FULL_MASK, A[j / G][j], gbase + (j % G));
@@ -174,10 +176,11 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             vj = x0 - bj;
             gj = rcp_fast(nrm * (nrm + fabs(x0)));
         }
-        gam[j] = gj;
-        beta[j] = bj;
-        inv_beta[j] = ib;
-        v0[j] = vj;
+        if (glane == 0) {
+            sGam[j] = gj;
+            sIb[j] = ib;
+            sV0[j] = vj;
+        }
         double dot[NC];
 #pragma unroll
         for (int l = j + 1; l < NC; l++) {
@@ -257,7 +260,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
                 double acc = (i == l) ? 1.0 : 0.0;
 #pragma unroll
                 for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
-                x[i] = (i <= l) ? acc * inv_beta[i] : 0.0;
+                x[i] = (i <= l) ? acc * sIb[i] : 0.0;
                 if (i <= l && l < K) {
                     colsum += fabs(sR[i * K + l]);
                     invsum += fabs(x[i]);
@@ -277,10 +280,10 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double acc = sQ[i];
 #pragma unroll
             for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], cs[c], acc);
-            cs[i] = acc * inv_beta[i];
+            cs[i] = acc * sIb[i];
         }
 #pragma unroll
-        for (int c = 0; c < K; c++) coeffs[c] = __ddiv_rn(cs[c], spow[c]);
+        for (int c = 0; c < K; c++) coeffs[c] = __ddiv_rn(cs[c], spow(c));
         if (centering) {
             value = coeffs[0];  // _ext.pyx:413-414
         } else {
@@ -301,7 +304,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double mono_t[K];
             eval_monos<DIM, DEG>(t, mono_t);
 #pragma unroll
-            for (int i = 0; i < K; i++) g[i] = __ddiv_rn(mono_t[i], spow[i]);
+            for (int i = 0; i < K; i++) g[i] = __ddiv_rn(mono_t[i], spow(i));
         }
         double z[K];
 #pragma unroll
@@ -309,7 +312,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             double acc = g[i];
 #pragma unroll
             for (int c = 0; c < i; c++) acc = fma(-sR[c * K + i], z[c], acc);
-            z[i] = acc * inv_beta[i];
+            z[i] = acc * sIb[i];
         }
         double yy[ROWS];
 #pragma unroll
@@ -325,19 +328,20 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         // move A into local memory)
         static_for<0, K>([&](auto jj) {
             constexpr int j = K - 1 - decltype(jj)::value;
+            const double vj = sV0[j];
             double pl = 0.0;
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) pl = fma(v0[j], yy[q], pl);
+                if (row_diag<G>(q, j, glane)) pl = fma(vj, yy[q], pl);
                 else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], yy[q], pl);
                 (void)i;
             }
-            const double td = gam[j] * group_sum<G>(pl);
+            const double td = sGam[j] * group_sum<G>(pl);
 #pragma unroll
             for (int q = 0; q < ROWS; q++) {
                 const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) yy[q] = fma(-td, v0[j], yy[q]);
+                if (row_diag<G>(q, j, glane)) yy[q] = fma(-td, vj, yy[q]);
                 else if (row_below<G>(q, j, glane)) yy[q] = fma(-td, A[q][j], yy[q]);
                 (void)i;
             }

@@ -142,7 +142,7 @@ struct GroupSmem {
 template <int G>
 __host__ __device__ inline size_t group_smem_bytes(int cap, int K) {
     return sizeof(RowTable<G>) + (size_t)cap * 4 * sizeof(int32_t) +
-           (size_t)(K * K + K) * sizeof(double) + 16;
+           (size_t)(K * K + 4 * K) * sizeof(double) + 16;
 }
 
 template <int G>
@@ -153,7 +153,7 @@ __device__ __forceinline__ GroupSmem<G> carve(char *base, int cap, int K) {
     gs.sR = reinterpret_cast<double *>(p);
     p += (size_t)K * K * sizeof(double);
     gs.sQ = reinterpret_cast<double *>(p);
-    p += (size_t)K * sizeof(double);
+    p += (size_t)4 * K * sizeof(double);  // sQ, then the reflector scalars (fit_rows)
     gs.rt = reinterpret_cast<RowTable<G> *>(p);
     p += sizeof(RowTable<G>);
     gs.id = reinterpret_cast<int32_t *>(p);
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kBlock) k_fit_many(fm_fit fp, const double *__
                                                      int32_t *__restrict__ stats) {
     constexpr int K = Monos<DIM, DEG>::K;
     int nfail = 0, first_fail = INT32_MAX;
-    __shared__ double sRs[kBlock / G][K * K + K];
+    __shared__ double sRs[kBlock / G][K * K + 4 * K];
     double *sR = sRs[threadIdx.x / G];
     double *sQ = sR + K * K;
     constexpr int GPW = 32 / G;
