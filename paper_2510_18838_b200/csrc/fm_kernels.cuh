@@ -237,13 +237,106 @@ struct BuildArgs {
     int32_t *stats;
 };
 
-template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
+// Inputs of one target of a build tile, staged one tile ahead on the slot
+// path (the dependent klist -> record/slots -> points chain is what the
+// build waits on; prefetching the next tile's records overlaps it with the
+// current tile's fit).
+template <int DIM, int ROWS>
+struct TileIn {
+    int64_t k;
+    PosInfo pi;
+    double t[DIM];
+    int32_t ids[ROWS], spos[ROWS];
+    int64_t off;
+};
+
+template <int DIM, int G, int ROWS, bool SOLVE>
+__device__ __forceinline__ void fetch_tile(const BuildArgs &b, int64_t ii, int64_t k, int glane,
+                                           TileIn<DIM, ROWS> &T) {
+    const bool act = ii < b.nk;
+    if (!act) k = 0;
+    T.k = k;
+    T.pi = act ? b.pos_info[k] : make_pos_info(0, 0, 0.0);
+#pragma unroll
+    for (int a = 0; a < DIM; a++) T.t[a] = act ? __ldg(b.pos_t + k * DIM + a) : 0.0;
+    // slot loads do not wait for m (in-bounds garbage past it is never used)
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        T.ids[q] = 0;
+        T.spos[q] = 0;
+        if (i < b.slot_cap) {
+            T.ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
+            T.spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
+        }
+    }
+    T.off = (!SOLVE && act) ? __ldg(b.offsets + k) : 0;
+}
+
+// One target of the build: support rows -> weights -> fit -> operator row
+// (or value).  A function, not a lambda: a non-inlined lambda capturing the
+// kernel arguments by reference puts them in a local-memory stack frame.
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
+__device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &b,
+                                          const GroupSmem<G> &gs, int lane, int glane,
+                                          bool active, int64_t k, int64_t tid,
+                                          const double (&t)[DIM], double r, int m,
+                                          const int32_t (&ids)[ROWS],
+                                          const int32_t (&spos)[ROWS], int64_t off, int &nfail,
+                                          int &first_fail) {
+    constexpr int K = Monos<DIM, DEG>::K;
+    bool valid[ROWS];
+    double p[ROWS][DIM], w[ROWS], f[ROWS];
+    const double inv_r = active ? 1.0 / r : 0.0;
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        valid[q] = i < m;
+        w[q] = 0.0;
+        f[q] = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
+        if (valid[q]) {
+            load_point<DIM>(s.sorted_pts, spos[q], p[q]);
+            const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
+            w[q] = fabs(rbf_fast(b.rbf_kind, b.rbf_a, r, inv_r, d));  // pointwise.py:301
+            if (SOLVE) f[q] = __ldg(b.src_val + ids[q]);
+        }
+    }
+    double y[ROWS], coeffs[K], value = 0.0;
+    const int st = fit_rows<DIM, DEG, G, ROWS, SOLVE>(b.fp, t, m, valid, p, w, f, lane, glane,
+                                                      gs.sR, gs.sQ, y, coeffs, value);
+    if (active) {
+        if (glane == 0) {
+            b.status[tid] = (uint8_t)st;
+            if (st != FM_FIT_OK) {
+                nfail++;
+                first_fail = min(first_fail, (int)tid);
+            }
+        }
+        if (SOLVE) {
+            if (glane == 0) b.values[tid] = st == FM_FIT_OK ? value : NAN;
+        } else {
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                if (valid[q]) {
+                    const int i = q * G + glane;
+                    b.col[off + i] = ids[q];
+                    b.val[off + i] = st == FM_FIT_OK ? y[q] : NAN;
+                }
+            }
+        }
+    }
+    __syncwarp();
+}
+
 #ifndef FM_BUILD_MINB8
 #define FM_BUILD_MINB8 4
 #endif
 #ifndef FM_BUILD_MINB8_R2
 #define FM_BUILD_MINB8_R2 4
 #endif
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
 __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MINB8_R2
                                           : (G == 8 && ROWS <= 4) ? FM_BUILD_MINB8
                                                                   : 1) k_build(SearchArgs s,
@@ -256,111 +349,74 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
     const int lane = threadIdx.x & 31, glane = lane & (G - 1);
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    // the next tile's klist entry is loaded one iteration ahead
-    int32_t k_next = (b.klist && warp * GPW + lane / G < b.nk) ? b.klist[warp * GPW + lane / G] : 0;
-    for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
-        const int64_t ii = tile * GPW + lane / G;
-        bool active = ii < b.nk;
-        const int64_t k = active ? (b.klist ? (int64_t)k_next : ii) : 0;
-        if (b.klist) {
-            const int64_t iin = ii + nwarps * GPW;
-            k_next = iin < b.nk ? b.klist[iin] : 0;
-        }
-        int64_t tid;
-        double t[DIM];
-        double r;
-        int m = 0;
-        if (FROM_SLOTS && b.pos_info) {
-            // per-position record of the select pass: loads indexed by k only
-            const PosInfo pi = active ? b.pos_info[k] : make_pos_info(0, 0, 0.0);
-            tid = pi.tid;
-            m = pi.m;
-            r = pi.r;
-#pragma unroll
-            for (int a = 0; a < DIM; a++) t[a] = active ? __ldg(b.pos_t + k * DIM + a) : 0.0;
-        } else {
-            tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
-            load_target<DIM>(s.targets, tid, active, t);
-            r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
-            if (FROM_SLOTS) m = active ? b.counts[tid] : 0;
-        }
-        if (FROM_SLOTS) {
+    const int64_t stride = nwarps * GPW;
+    const bool staged = FROM_SLOTS && b.pos_info != nullptr;
+    auto kof = [&](int64_t ii) -> int64_t {
+        return b.klist ? (ii < b.nk ? (int64_t)b.klist[ii] : 0) : ii;
+    };
+
+    if (staged) {
+        // slot path: records, slots and row offsets of tile n+1 are in flight
+        // while tile n is fitted; klist runs two tiles ahead
+        const int64_t ii0 = warp * GPW + lane / G;
+        TileIn<DIM, ROWS> cur;
+        fetch_tile<DIM, G, ROWS, SOLVE>(b, ii0, kof(ii0), glane, cur);
+        int64_t k_next = kof(ii0 + stride);
+        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
+            const int64_t ii = tile * GPW + lane / G;
+            TileIn<DIM, ROWS> nxt;
+            fetch_tile<DIM, G, ROWS, SOLVE>(b, ii + stride, k_next, glane, nxt);
+            k_next = kof(ii + 2 * stride);
+            bool active = ii < b.nk;
+            int m = cur.pi.m;
             if (m > b.slot_cap) {  // overflow: built by the rescan launch
                 active = false;
                 m = 0;
             }
-        } else {
-            m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r, active,
-                                       lane, glane, *gs.rt, gs.id, gs.pos, gs.sid, gs.spos, b.cap);
-            if (m > b.cap) m = b.cap;  // host sizes cap >= max count
+            build_one<DIM, DEG, G, ROWS, SOLVE>(s, b, gs, lane, glane, active, cur.k, cur.pi.tid,
+                                                cur.t, cur.pi.r, m, cur.ids, cur.spos, cur.off,
+                                                nfail, first_fail);
+            cur = nxt;
         }
-        bool valid[ROWS];
-        double p[ROWS][DIM], w[ROWS], f[ROWS];
-        int32_t ids[ROWS], spos[ROWS];
-        if (FROM_SLOTS) {
-            // slot loads do not wait for m (in-bounds garbage past it is never
-            // used), so they overlap the position-record loads
-#pragma unroll
-            for (int q = 0; q < ROWS; q++) {
-                const int i = q * G + glane;
-                ids[q] = 0;
-                spos[q] = 0;
-                if (i < b.slot_cap) {
-                    ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
-                    spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
+    } else {
+        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
+            const int64_t ii = tile * GPW + lane / G;
+            bool active = ii < b.nk;
+            const int64_t k = active ? kof(ii) : 0;
+            const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
+            double t[DIM];
+            load_target<DIM>(s.targets, tid, active, t);
+            const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
+            int m = 0;
+            int32_t ids[ROWS], spos[ROWS];
+            if (FROM_SLOTS) {
+                m = active ? b.counts[tid] : 0;
+                if (m > b.slot_cap) {  // overflow: built by the rescan launch
+                    active = false;
+                    m = 0;
                 }
-            }
-        }
-        const double inv_r = active ? 1.0 / r : 0.0;
-#pragma unroll
-        for (int q = 0; q < ROWS; q++) {
-            const int i = q * G + glane;
-            valid[q] = i < m;
-            if (!FROM_SLOTS) ids[q] = 0;
-            w[q] = 0.0;
-            f[q] = 0.0;
-#pragma unroll
-            for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
-            if (valid[q]) {
-                int32_t pos;
-                if (FROM_SLOTS) {
-                    pos = spos[q];
-                } else {
-                    ids[q] = gs.sid[i];
-                    pos = gs.spos[i];
-                }
-                load_point<DIM>(s.sorted_pts, pos, p[q]);
-                const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
-                w[q] = fabs(rbf_fast(b.rbf_kind, b.rbf_a, r, inv_r, d));  // pointwise.py:301
-                if (SOLVE) f[q] = __ldg(b.src_val + ids[q]);
-            }
-        }
-        double y[ROWS], coeffs[K], value = 0.0;
-        const int st = fit_rows<DIM, DEG, G, ROWS, SOLVE>(b.fp, t, m, valid, p, w, f, lane, glane,
-                                                          gs.sR, gs.sQ, y, coeffs, value);
-        if (active) {
-            if (glane == 0) {
-                b.status[tid] = (uint8_t)st;
-                if (st != FM_FIT_OK) {
-                    nfail++;
-                    first_fail = min(first_fail, (int)tid);
-                }
-            }
-            if (SOLVE) {
-                if (glane == 0) b.values[tid] = st == FM_FIT_OK ? value : NAN;
-            } else {
-                const int64_t off = b.offsets[k];
 #pragma unroll
                 for (int q = 0; q < ROWS; q++) {
-                    if (valid[q]) {
-                        const int i = q * G + glane;
-                        b.col[off + i] = ids[q];
-                        b.val[off + i] = st == FM_FIT_OK ? y[q] : NAN;
-                    }
+                    const int i = q * G + glane;
+                    ids[q] = i < m ? __ldg(b.slot_id + k * b.slot_cap + i) : 0;
+                    spos[q] = i < m ? __ldg(b.slot_pos + k * b.slot_cap + i) : 0;
+                }
+            } else {
+                m = collect_sorted<DIM, G>(s.g, s.cell_start, s.sorted_pts, s.sorted_ids, t, r,
+                                           active, lane, glane, *gs.rt, gs.id, gs.pos, gs.sid,
+                                           gs.spos, b.cap);
+                if (m > b.cap) m = b.cap;  // host sizes cap >= max count
+#pragma unroll
+                for (int q = 0; q < ROWS; q++) {
+                    const int i = q * G + glane;
+                    ids[q] = i < m ? gs.sid[i] : 0;
+                    spos[q] = i < m ? gs.spos[i] : 0;
                 }
             }
+            const int64_t off = (!SOLVE && active) ? b.offsets[k] : 0;
+            build_one<DIM, DEG, G, ROWS, SOLVE>(s, b, gs, lane, glane, active, k, tid, t, r, m,
+                                                ids, spos, off, nfail, first_fail);
         }
-        __syncwarp();
     }
     if (b.stats) warp_flush_pair(b.stats, nfail, first_fail);
 }
