@@ -124,9 +124,10 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
  * (device).  The `bbox` of locate.py:151. */
 int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t stream);
 
-/* Processing order of targets (cell order of the source grid) for locality.
- * Results never depend on it; perm[k] = target processed k-th. */
-size_t fm_order_workspace(int64_t nt, int64_t ncell);
+/* Processing order of targets for locality: the source grid's cells in
+ * blocks of 8x8 (2-D), 4x4x4 (3-D) or 2^dim cells, block-major.  Results
+ * never depend on it; perm[k] = target processed k-th. */
+size_t fm_order_workspace(int64_t nt, const fm_grid *grid);
 int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
                     void *workspace, size_t workspace_bytes, fm_stream_t stream);
 

@@ -24,6 +24,53 @@ __device__ __forceinline__ int64_t cell_key(const GridDev &g, const double *p) {
     return c;
 }
 
+// Processing-order key of a target: cells grouped into blocks of
+// kOrderBlock^DIM cells (block-major, row-major inside a block), so that a
+// run of consecutive targets covers a compact patch of the domain rather
+// than a one-cell-high strip -- neighbouring targets share sources (L1 /
+// shared-memory reuse in the build and the apply).  Dense in
+// [0, order_keys(grid)).
+template <int DIM>
+struct OrderBlock {
+    static constexpr int B = DIM == 1 ? 1 : DIM == 2 ? 8 : DIM == 3 ? 4 : 2;
+};
+
+template <int DIM>
+__device__ __forceinline__ int64_t order_key(const GridDev &g, const double *p) {
+    constexpr int B = OrderBlock<DIM>::B;
+    int64_t blk = 0, bstride = 1, loc = 0, lstride = 1;
+#pragma unroll
+    for (int a = 0; a < DIM; a++) {
+        const int64_t c = cell_of(p[a], g.lo[a], g.inv_d[a], g.n[a]);
+        blk += (c / B) * bstride;
+        bstride *= (g.n[a] + B - 1) / B;
+        loc += (c % B) * lstride;
+        lstride *= B;
+    }
+    return blk * lstride + loc;
+}
+
+static int64_t order_keys(const fm_grid *grid) {
+    int B = grid->dim == 1 ? 1 : grid->dim == 2 ? 8 : grid->dim == 3 ? 4 : 2;
+    int64_t nk = 1;
+    for (int a = 0; a < grid->dim; a++) nk *= ((grid->n[a] + B - 1) / B) * B;
+    return nk;
+}
+
+template <int DIM>
+__global__ void k_order_keys(GridDev g, const double *__restrict__ pts, int64_t n,
+                             int32_t *__restrict__ keys, int32_t *__restrict__ counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double p[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; a++) p[a] = pts[i * DIM + a];
+        const int32_t c = (int32_t)order_key<DIM>(g, p);
+        keys[i] = c;
+        atomicAdd(&counts[c], 1);
+    }
+}
+
 template <int DIM>
 __global__ void k_cell_keys(GridDev g, const double *__restrict__ pts, int64_t n,
                             int32_t *__restrict__ keys, int32_t *__restrict__ counts) {
@@ -147,10 +194,13 @@ __global__ void k_bbox_final(const unsigned long long *acc, int dim, double *loh
 
 template <int DIM>
 static int launch_keys(const GridDev &g, const double *pts, int64_t n, int32_t *keys,
-                       int32_t *counts, cudaStream_t s) {
+                       int32_t *counts, cudaStream_t s, bool order = false) {
     const int threads = 256;
     const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
-    if (blocks) k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
+    if (blocks && order)
+        k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
+    else if (blocks)
+        k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -251,16 +301,20 @@ int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t str
     return FM_OK;
 }
 
-size_t fm_order_workspace(int64_t nt, int64_t ncell) { return fm_grid_workspace(nt, ncell) + align256(sizeof(int32_t) * (size_t)(ncell + 1)); }
+size_t fm_order_workspace(int64_t nt, const fm_grid *grid) {
+    if (!grid || grid->dim < 1 || grid->dim > kMaxDim) return 0;
+    const int64_t nk = order_keys(grid);
+    return fm_grid_workspace(nt, nk) + align256(sizeof(int32_t) * (size_t)(nk + 1));
+}
 
 int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
                     void *workspace, size_t workspace_bytes, fm_stream_t stream) {
     if (!grid || grid->dim < 1 || grid->dim > kMaxDim || nt < 0 || grid->ncell < 1)
         return FM_ERR_ARG;
-    if (nt >= (int64_t)INT32_MAX || grid->ncell >= (int64_t)INT32_MAX) return FM_ERR_UNSUPPORTED;
-    if (workspace_bytes < fm_order_workspace(nt, grid->ncell)) return FM_ERR_WORKSPACE;
+    const int64_t ncell = order_keys(grid);  // key range of the blocked order
+    if (nt >= (int64_t)INT32_MAX || ncell >= (int64_t)INT32_MAX) return FM_ERR_UNSUPPORTED;
+    if (workspace_bytes < fm_order_workspace(nt, grid)) return FM_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t ncell = grid->ncell;
     char *w = (char *)workspace;
     int32_t *keys = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)nt);
@@ -276,11 +330,11 @@ int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int3
     cudaMemsetAsync(fill, 0, sizeof(int32_t) * (size_t)ncell, s);
     int rc;
     switch (grid->dim) {
-    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s); break;
-    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s); break;
-    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s); break;
-    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s); break;
-    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s); break;
+    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s, true); break;
+    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s, true); break;
+    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s, true); break;
+    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s, true); break;
+    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s, true); break;
     }
     if (rc) return rc;
     rc = exclusive_scan<int32_t, int32_t>(counts, ncell, start, scan_ws,

@@ -97,7 +97,7 @@ class SourceCloud:
         L = _lib.lib()
         nt = targets.shape[0]
         perm = _empty(nt, torch.int32, targets.device)
-        ws_bytes = L.fm_order_workspace(nt, self.geom.ncell)
+        ws_bytes = L.fm_order_workspace(nt, ctypes.byref(self.grid))
         ws = _workspace(ws_bytes, targets.device)
         check(L.fm_target_order(ctypes.byref(self.grid), ptr(targets), nt, ptr(perm), ptr(ws),
                                 ws_bytes, _stream()), "fm_target_order")

@@ -497,3 +497,61 @@ def test_extension_multicomponent_apply_equals_columns():
                                  src, V, 2, 0.0, True)
     assert _rel(Y, want) < VALUE_RTOL
     assert _rel(P.fit_point_cloud(src, V, tg, spec), want) < VALUE_RTOL
+
+
+def _apply_direct(row_lens, ns, C, seed, local=True):
+    """fm_apply on a synthetic CSR (rows in stored order, perm reversed)
+    against a float64 numpy reference; exercises the tiled kernel's staged
+    path (local columns), its fallbacks (tile streams > 2048 nonzeros, > 512
+    distinct columns) and the direct kernels (C != 8)."""
+    import torch
+
+    from paper_2510_18838_b200 import _lib as L
+    from paper_2510_18838_b200.device import _stream
+
+    rng = np.random.default_rng(seed)
+    nt = len(row_lens)
+    off = np.zeros(nt + 1, np.int64)
+    off[1:] = np.cumsum(row_lens)
+    nnz = int(off[-1])
+    if local:  # columns near the row's position (neighbouring rows share)
+        base = (np.repeat(np.arange(nt), row_lens) * ns) // max(nt, 1)
+        col = np.clip(base + rng.integers(-20, 21, nnz), 0, ns - 1).astype(np.int32)
+    else:
+        col = rng.integers(0, ns, nnz).astype(np.int32)
+    val = rng.standard_normal(nnz)
+    perm = np.arange(nt)[::-1].astype(np.int32).copy()
+    X = rng.standard_normal((ns, C))
+    want = np.zeros((nt, C))
+    for k in range(nt):
+        sl = slice(off[k], off[k + 1])
+        want[perm[k]] = val[sl] @ X[col[sl]]
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    Y = torch.full((nt, C), np.nan, dtype=torch.float64, device="cuda")
+    off_d, col_d, val_d, perm_d, X_d = d(off), d(col), d(val), d(perm), d(X)
+    L.check(L.lib().fm_apply(nt, L.ptr(off_d), L.ptr(col_d), L.ptr(val_d), L.ptr(perm_d),
+                             L.ptr(X_d), C, L.ptr(Y), _stream()), "fm_apply")
+    got = Y.cpu().numpy()
+    scale = (np.abs(val).max() if nnz else 1.0) * np.abs(X).max() * max(int(row_lens.max()), 1)
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 1e-13 * scale
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C", [1, 2, 4, 8, 16, 3])
+def test_apply_local_rows(C):
+    rng = np.random.default_rng(5)
+    _apply_direct(rng.integers(0, 40, 5000), 3000, C, 11)
+
+
+@pytest.mark.gpu
+def test_apply_tiled_fallbacks():
+    rng = np.random.default_rng(6)
+    lens = rng.integers(5, 30, 3000)
+    lens[640:704] = 100          # one 64-row tile with 6400 nonzeros (> 2048 staged)
+    lens[1000] = 5000            # a single very long row
+    lens[2000:2010] = 0          # empty rows
+    _apply_direct(lens, 100000, 8, 12, local=True)
+    _apply_direct(rng.integers(20, 30, 3000), 100000, 8, 13, local=False)  # > 512 distinct/tile
+    _apply_direct(np.array([3]), 10, 8, 14)       # one row, partial tile
+    _apply_direct(np.zeros(70, np.int64), 10, 8, 15)  # all rows empty
