@@ -104,195 +104,6 @@ __global__ void __launch_bounds__(256) k_apply(int64_t nrows, const int64_t *__r
     }
 }
 
-// ---- tiled apply: one CTA per tile of kTileRows consecutive stored rows.
-// Neighbouring targets share most of their sources, so the tile's gather is
-// deduplicated in shared memory: the tile's (col, val) stream is staged
-// (prefetched into registers one tile ahead), the distinct columns are
-// found with a shared-memory hash table and compacted, each distinct X row
-// is read from HBM/L2 once into shared memory, and the rows accumulate from
-// there in the stored (j ascending) order -- bitwise the same sums as the
-// direct kernel.  A tile whose stream or distinct set does not fit falls
-// back to the direct per-row gather.
-constexpr int kTileRows = 64;
-constexpr int kTileNnz = 2048;   // staged nonzeros per tile
-constexpr int kTileHash = 1024;  // hash slots (power of two)
-constexpr int kTileUniq = 512;   // distinct X rows staged per tile
-constexpr int kTileThreads = 256;
-constexpr int kTileNzPer = kTileNnz / kTileThreads;
-
-template <int L>
-__global__ void __launch_bounds__(kTileThreads, 3)
-    k_apply_tiled(int64_t nrows, const int64_t *__restrict__ row_off,
-                  const int32_t *__restrict__ col, const double *__restrict__ val,
-                  const int32_t *__restrict__ row_target, const double *__restrict__ X,
-                  double *__restrict__ Y) {
-    constexpr int C = 2 * L;
-    constexpr int RPW = 32 / L;  // rows per warp pass
-    extern __shared__ __align__(16) char smem[];
-    double *s_X = reinterpret_cast<double *>(smem);  // kTileUniq * C
-    double *s_val = s_X + kTileUniq * C;              // kTileNnz
-    int64_t *s_off = reinterpret_cast<int64_t *>(s_val + kTileNnz);  // kTileRows + 1
-    int32_t *s_key = reinterpret_cast<int32_t *>(s_off + kTileRows + 1);  // kTileHash
-    int32_t *s_uid = s_key + kTileHash;                                    // kTileUniq
-    int32_t *s_wsum = s_uid + kTileUniq;                                   // 8
-    uint16_t *s_cid = reinterpret_cast<uint16_t *>(s_wsum + kTileThreads / 32);  // kTileHash
-    uint16_t *s_pos = s_cid + kTileHash;                                   // kTileNnz
-    __shared__ int s_full[1];
-    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-    const int rr = lane / L, li = lane % L;
-    const int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
-    for (int i = tid; i < kTileHash; i += kTileThreads) s_key[i] = -1;
-
-    // register prefetch of a tile's (col, val) stream
-    int32_t pc[kTileNzPer];
-    double pv[kTileNzPer];
-    auto fetch = [&](int64_t tile, int64_t &tb, int64_t &te) {
-        tb = te = 0;
-        if (tile < ntiles) {
-            const int64_t r0 = tile * kTileRows;
-            const int64_t r1 = r0 + kTileRows < nrows ? r0 + kTileRows : nrows;
-            tb = __ldg(row_off + r0);
-            te = __ldg(row_off + r1);
-        }
-        const int64_t n = te - tb;
-#pragma unroll
-        for (int u = 0; u < kTileNzPer; u++) {
-            const int i = u * kTileThreads + tid;
-            pc[u] = (n <= kTileNnz && i < n) ? __ldg(col + tb + i) : -1;
-            pv[u] = (n <= kTileNnz && i < n) ? __ldg(val + tb + i) : 0.0;
-        }
-    };
-    int64_t tb, te;
-    fetch(blockIdx.x, tb, te);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * kTileRows;
-        const int nr = (int)(r0 + kTileRows < nrows ? kTileRows : nrows - r0);
-        const int64_t n = te - tb;
-        for (int i = tid; i <= nr; i += kTileThreads) s_off[i] = __ldg(row_off + r0 + i) - tb;
-        if (tid == 0) s_full[0] = 0;
-        __syncthreads();
-        bool staged = n <= kTileNnz;
-        // ---- A: stage vals, hash the columns
-        if (staged) {
-#pragma unroll
-            for (int u = 0; u < kTileNzPer; u++) {
-                const int i = u * kTileThreads + tid;
-                if (pc[u] >= 0) {
-                    s_val[i] = pv[u];
-                    unsigned h = ((unsigned)pc[u] * 2654435761u) >> 22;  // 10 bits
-                    for (int probe = 0;; probe++) {
-                        const int prev = atomicCAS(&s_key[h], -1, pc[u]);
-                        if (prev == -1 || prev == pc[u]) break;
-                        if (probe == kTileHash) {  // table full: direct gather
-                            s_full[0] = 1;
-                            break;
-                        }
-                        h = (h + 1) & (kTileHash - 1);
-                    }
-                    s_pos[i] = (uint16_t)h;
-                }
-            }
-        }
-        int64_t ntb, nte;
-        fetch(tile + gridDim.x, ntb, nte);  // next tile's stream in flight
-        __syncthreads();
-        // ---- B: compact the occupied slots (block scan over 4 slots/thread)
-        int occ[kTileHash / kTileThreads], cnt = 0;
-#pragma unroll
-        for (int u = 0; u < kTileHash / kTileThreads; u++) {
-            occ[u] = staged && s_key[tid * (kTileHash / kTileThreads) + u] >= 0;
-            cnt += occ[u];
-        }
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FM_FULL_MASK, incl, o);
-            if (lane >= o) incl += v;
-        }
-        if (lane == 31) s_wsum[wib] = incl;
-        __syncthreads();
-        int wbase = 0, nuniq = 0;
-#pragma unroll
-        for (int w = 0; w < kTileThreads / 32; w++) {
-            const int v = s_wsum[w];
-            wbase += w < wib ? v : 0;
-            nuniq += v;
-        }
-        staged = staged && nuniq <= kTileUniq && !s_full[0];
-        if (staged) {
-            int c = wbase + incl - cnt;
-#pragma unroll
-            for (int u = 0; u < kTileHash / kTileThreads; u++) {
-                const int h = tid * (kTileHash / kTileThreads) + u;
-                if (occ[u]) {
-                    s_cid[h] = (uint16_t)c;
-                    s_uid[c] = s_key[h];
-                    c++;
-                }
-            }
-        }
-        __syncthreads();
-        if (staged) {
-            // ---- C: distinct X rows -> shared memory; slots -> compact ids
-            for (int c = tid / L; c < nuniq; c += kTileThreads / L) {
-                const double2 x2 =
-                    __ldg(reinterpret_cast<const double2 *>(X + (int64_t)s_uid[c] * C) + li);
-                reinterpret_cast<double2 *>(s_X + c * C)[li] = x2;
-            }
-            for (int i = tid; i < n; i += kTileThreads) s_pos[i] = s_cid[s_pos[i]];
-        }
-        __syncthreads();
-        for (int i = tid; i < kTileHash; i += kTileThreads) s_key[i] = -1;
-        // ---- D: rows (L lanes per row, 2 components per lane), j ascending
-        for (int rl = wib * RPW + rr; rl < kTileRows; rl += (kTileThreads / 32) * RPW) {
-            if (rl >= nr) continue;
-            const int j0 = (int)s_off[rl], j1 = (int)s_off[rl + 1];
-            double a0 = 0.0, a1 = 0.0;
-            if (staged) {
-                for (int j = j0; j < j1; j++) {
-                    const double v = s_val[j];
-                    const double2 x2 = reinterpret_cast<const double2 *>(s_X + s_pos[j] * C)[li];
-                    a0 = fma(v, x2.x, a0);
-                    a1 = fma(v, x2.y, a1);
-                }
-            } else {
-                for (int j = j0; j < j1; j++) {
-                    const double v = __ldg(val + tb + j);
-                    const double2 x2 = __ldg(
-                        reinterpret_cast<const double2 *>(X + (int64_t)__ldg(col + tb + j) * C) + li);
-                    a0 = fma(v, x2.x, a0);
-                    a1 = fma(v, x2.y, a1);
-                }
-            }
-            const int64_t r = r0 + rl;
-            const int64_t t = row_target ? (int64_t)row_target[r] : r;
-            reinterpret_cast<double2 *>(Y + t * C)[li] = make_double2(a0, a1);
-        }
-        __syncthreads();
-        tb = ntb;
-        te = nte;
-    }
-}
-
-inline size_t tiled_smem_bytes(int C) {
-    return sizeof(double) * ((size_t)kTileUniq * C + kTileNnz + kTileRows + 1) +
-           sizeof(int32_t) * (kTileHash + kTileUniq + kTileThreads / 32) +
-           sizeof(uint16_t) * (kTileHash + kTileNnz);
-}
-
-template <int L>
-static int launch_apply_tiled(int64_t nrows, const int64_t *row_off, const int32_t *col,
-                              const double *val, const int32_t *row_target, const double *X,
-                              double *Y, cudaStream_t st) {
-    const int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kSMs * 3));
-    const size_t sm = tiled_smem_bytes(2 * L);
-    cudaFuncSetAttribute(k_apply_tiled<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_apply_tiled<L><<<blocks, kTileThreads, sm, st>>>(nrows, row_off, col, val, row_target, X, Y);
-    FM_CHECK_LAUNCH();
-    return FM_OK;
-}
-
 // any C: one thread per (stored row, component)
 __global__ void k_apply_generic(int64_t nrows, const int64_t *__restrict__ row_off,
                                 const int32_t *__restrict__ col, const double *__restrict__ val,
@@ -640,11 +451,7 @@ int fm_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const doubl
     case 1: return launch_apply<1, 1>(nt, row_off, col, val, row_order, X, Y, st);
     case 2: if (a16) return launch_apply<1, 2>(nt, row_off, col, val, row_order, X, Y, st); break;
     case 4: if (a16) return launch_apply<2, 2>(nt, row_off, col, val, row_order, X, Y, st); break;
-#ifdef FM_APPLY_DIRECT8
     case 8: if (a16) return launch_apply<4, 2>(nt, row_off, col, val, row_order, X, Y, st); break;
-#else
-    case 8: if (a16) return launch_apply_tiled<4>(nt, row_off, col, val, row_order, X, Y, st); break;
-#endif
     case 16: if (a16) return launch_apply<8, 2>(nt, row_off, col, val, row_order, X, Y, st); break;
     default: break;
     }
