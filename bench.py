@@ -13,8 +13,10 @@ One step = the whole hot path over that batch, inputs resident in HBM:
   -> CSR scan -> fused fill + C4 weights + QR fit (operator build)
   -> 8-component operator apply   [-> NCCL all-gather of the target field, N>1]
 value = targets mapped per second (whole job).  `e2e` = the same through the
-public API (PreparedTransfer(...).apply(...)) with host inputs: H2D of
-sources/targets/field and D2H of the result inside the timed region.
+public one-shot API (fit_point_cloud(sources, field, targets, spec),
+pointwise.py:434) with pinned host tensors: H2D of sources/targets/field and
+D2H of the result inside the timed region (the field's H2D overlaps the
+selection and operator build on a side stream).
 
 N>1 (torchrun): weak scaling -- every rank maps its own 1,000,519 targets
 (the target disk rotated by a rank-dependent angle) against the replicated
@@ -186,10 +188,13 @@ def fit_flops(counts, k):
 
 # ------------------------------------------------------------ b200 arm
 # kernels launched by one device step (our own, counted from the launch
-# sequence in device.py / libfieldmap.so): source bbox 3, grid build 7,
-# target order 5, target bbox 3, select 2, ordered offsets 4, operator build 2,
-# apply 1 (+1 build launch per step if some support overflows its slot)
-LAUNCHES_PER_STEP = 3 + 7 + 5 + 3 + 2 + 4 + 2 + 1
+# sequence in device.py / libfieldmap.so and checked against the ncu launch
+# list): source bbox 3, grid build 7, target order 5, target bbox 3, select 2,
+# ordered offsets + size buckets 4, operator build 1 + one per non-empty size
+# bucket (+1 if some support overflows its slot), apply 1
+def launches_per_step(sel):
+    buckets = int(np.count_nonzero(sel.bucket_count)) if sel.bucket_count is not None else 1
+    return 3 + 7 + 5 + 3 + 2 + 4 + 1 + buckets + (1 if sel.n_overflow else 0) + 1
 
 
 def b200_step(src_d, tgt_d, X_d, spec, marks):
@@ -295,25 +300,28 @@ def run_b200(args, rank, world, local_rank):
         src_h = torch.from_numpy(src).pin_memory()
         tgt_h = torch.from_numpy(tgt).pin_memory()
         X_h = torch.from_numpy(X).pin_memory()
-        for _ in range(max(1, args.warmup // 2)):
-            P.PreparedTransfer(src_h, tgt_h, spec).apply(X_h)
+        def e2e_step():
+            if world > 1:
+                # sharded public API: this rank's rows, then the NCCL all-gather
+                # of the full target field, then D2H
+                Yd = P.fit_point_cloud(src_h, X_h.to("cuda", non_blocking=True), tgt_h, spec)
+                Yf = gather_target_field(Yd, nt_local * world)
+                Yh = torch.empty(Yf.shape, dtype=Yf.dtype, pin_memory=True)
+                Yh.copy_(Yf, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return Yh.numpy()
+            # one-shot transfer of the 8-component field (pointwise.py:434):
+            # host pinned buffers in, pinned host result out
+            return P.fit_point_cloud(src_h, X_h, tgt_h, spec).numpy()
+
+        for _ in range(max(3, args.warmup)):
+            e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            pt = P.PreparedTransfer(src_h, tgt_h, spec)
-            if world > 1:
-                # sharded public API: this rank's rows, then the NCCL all-gather
-                # of the full target field, then D2H
-                Yd = pt.apply(X_h.to("cuda", non_blocking=True))
-                Yf = gather_target_field(Yd, nt_local * world)
-                Yh = torch.empty(Yf.shape, dtype=Yf.dtype, pin_memory=True)
-                Yh.copy_(Yf, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-            else:
-                Yh = pt.apply(X_h)
-            Yh = Yh.numpy()
+            Yh = e2e_step()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -345,7 +353,7 @@ def run_b200(args, rank, world, local_rank):
             " + NCCL all-gather of the target field" if world > 1 else ""),
             l2="flushed between timed steps (256 MiB write)"),
         "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
-        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "gpu_launches": launches_per_step(cnt) * args.steps,
         "roofline": {
             "kernel": "k_build (C4 weights + Householder QR + operator row, supports from k_select)",
             "bound": "fp64",

@@ -463,7 +463,14 @@ class PreparedTransfer:
 def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=None, mesh=None,
                     source_location="vertices", threads=1):
     """Fit a value at each target from a scattered source point cloud
-    (pointwise.py:434-451)."""
+    (pointwise.py:434-451).  numpy in -> numpy out.  torch tensors in: CUDA
+    tensors -> CUDA tensor out (nothing copied to the host); host tensors
+    (pinned: asynchronous copies) -> pinned host tensor out, with the field's
+    host->device copy on a side stream overlapping the whole selection and
+    operator build."""
+    if any(isinstance(a, torch.Tensor) for a in (source_points, source_values, target_points)):
+        return _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec,
+                                        grid, mesh)
     src_xy = _as_points(source_points)
     src_vals = np.ascontiguousarray(source_values, dtype=np.float64)
     if src_xy.shape[0] == 0:
@@ -484,6 +491,51 @@ def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=N
     if int(stats[0].item()) > 0:
         plan.raise_fit_error(op.status)
     return op.apply(D.to_device(src_vals)).cpu().numpy()
+
+
+def _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec, grid, mesh):
+    as_t = lambda a: a if isinstance(a, torch.Tensor) else torch.from_numpy(  # noqa: E731
+        np.ascontiguousarray(a, dtype=np.float64))
+    sp, sv, tp = as_t(source_points), as_t(source_values), as_t(target_points)
+    host_out = not sv.is_cuda
+    if sp.shape[0] == 0:
+        raise InsufficientSourcesError("no source points")
+    if sp.shape[0] != sv.shape[0]:
+        raise FieldError("source points and values disagree in length")
+    _check_patch(fitspec, mesh)
+    main = torch.cuda.current_stream()
+    side = _copy_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        X = D.to_device(sv)  # async when pinned; overlaps everything below
+    src_d = D.to_device(sp)
+    tgt_d = D.to_device(tp).reshape(-1, src_d.shape[1])
+    if tgt_d.shape[0] == 0:
+        main.wait_stream(side)
+        Y = torch.empty((0,) + tuple(sv.shape[1:]), dtype=torch.float64, device=src_d.device)
+    else:
+        plan = _Plan(src_d, tgt_d, fitspec, grid)
+        if sv.ndim == 1:
+            main.wait_stream(side)
+            X.record_stream(main)
+            Y, status, stats = plan.transfer_scalar(X)
+            bad = stats
+        else:
+            op, bad = plan.build_operator()
+            status = op.status
+            main.wait_stream(side)
+            X.record_stream(main)
+            Y = op.apply(X)
+    if host_out:
+        out = torch.empty(Y.shape, dtype=Y.dtype, pin_memory=True)
+        out.copy_(Y, non_blocking=True)
+    else:
+        out = Y
+    if tgt_d.shape[0] and int(bad[0].item()) > 0:
+        plan.raise_fit_error(status)
+    if host_out:
+        main.synchronize()
+    return out
 
 
 def transfer_pointwise(source_field, target_points, fitspec, grid=None, threads=1):

@@ -7,4 +7,4 @@ timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo bench=$? >> g
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 ; echo launches=$? >> gpurun_out/status_$TAG.txt
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_build|k_select|k_apply" -c 3 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncufull=$? >> gpurun_out/status_$TAG.txt
+# (the ncu --set full capture is a separate gpurun call: scripts/gpu_ncu_only.sh)

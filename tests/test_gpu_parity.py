@@ -555,3 +555,30 @@ def test_apply_tiled_fallbacks():
     _apply_direct(rng.integers(20, 30, 3000), 100000, 8, 13, local=False)  # > 512 distinct/tile
     _apply_direct(np.array([3]), 10, 8, 14)       # one row, partial tile
     _apply_direct(np.zeros(70, np.int64), 10, 8, 15)  # all rows empty
+
+
+@pytest.mark.gpu
+def test_fit_point_cloud_tensor_paths():
+    """torch inputs: pinned host tensors -> pinned host tensor, CUDA tensors
+    -> CUDA tensor; same values as the numpy path (scalar and 8 components)."""
+    import torch
+
+    src, tg, vals, h = _c1()
+    V = synth.sincos_field(src, 8)
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(2 * h))
+    for field in (vals, V):
+        want = P.fit_point_cloud(src, field, tg, spec)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        got_h = P.fit_point_cloud(pin(src), pin(field), pin(tg), spec)
+        assert isinstance(got_h, torch.Tensor) and not got_h.is_cuda and got_h.is_pinned()
+        assert np.array_equal(got_h.numpy(), want)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        got_d = P.fit_point_cloud(cu(src), cu(field), cu(tg), spec)
+        assert got_d.is_cuda
+        assert np.array_equal(got_d.cpu().numpy(), want)
+    with pytest.raises(P.FieldError):
+        P.fit_point_cloud(torch.from_numpy(src), torch.ones(3, dtype=torch.float64),
+                          torch.from_numpy(tg), spec)
+    empty = P.fit_point_cloud(torch.from_numpy(src), torch.from_numpy(V),
+                              torch.zeros((0, 2), dtype=torch.float64), spec)
+    assert tuple(empty.shape) == (0, 8)
