@@ -504,12 +504,14 @@ def _fit_point_cloud_tensors(source_points, source_values, target_points, fitspe
         raise FieldError("source points and values disagree in length")
     _check_patch(fitspec, mesh)
     main = torch.cuda.current_stream()
+    # the geometry goes first (the pipeline starts on it); the field's copy
+    # follows on a side stream and overlaps the selection and build
+    src_d = D.to_device(sp)
+    tgt_d = D.to_device(tp).reshape(-1, src_d.shape[1])
     side = _copy_stream()
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        X = D.to_device(sv)  # async when pinned; overlaps everything below
-    src_d = D.to_device(sp)
-    tgt_d = D.to_device(tp).reshape(-1, src_d.shape[1])
+        X = D.to_device(sv)  # async when pinned
     if tgt_d.shape[0] == 0:
         main.wait_stream(side)
         Y = torch.empty((0,) + tuple(sv.shape[1:]), dtype=torch.float64, device=src_d.device)
