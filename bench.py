@@ -180,6 +180,19 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+def ncu_traffic():
+    """DRAM bytes per kernel from the committed ncu --set full capture
+    (profiles/traffic_*.json, newest round), or {}."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_*.json")))
+    if not paths:
+        return {}
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    d["file"] = os.path.relpath(paths[-1], ROOT)
+    return d
+
+
 def fit_flops(counts, k):
     """F(m,k) = 2mk^2 - (2/3)k^3 + 6mk + k^2 + m per target."""
     m = counts.astype(np.float64)
@@ -292,6 +305,7 @@ def run_b200(args, rank, world, local_rank):
     C = X.shape[1]
     apply_bytes = op.algorithmic_bytes(C)
     peaks = measured_peaks()
+    traffic = ncu_traffic()
     fp64_peak = D.fp64_probe() if rank == 0 else None
 
     # e2e through the public API with host (pinned) buffers
@@ -361,7 +375,8 @@ def run_b200(args, rank, world, local_rank):
             "peak": fp64_peak,
             "unit": "TFLOP/s",
             "frac": (flops / (build_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
-            "traffic": None,
+            "traffic": traffic.get("k_build_per_step"),
+            "traffic_unit": f"DRAM bytes per step, ncu ({traffic.get('file')})",
             "note": "algorithmic FP64 flops F(m,k) summed over this step's supports; peak = "
                     "DFMA-chain probe measured in this run (MEASURED_PEAKS.json has no FP64 "
                     "figure); the build is issue/latency bound, not FP64 bound",
@@ -373,7 +388,8 @@ def run_b200(args, rank, world, local_rank):
             "peak": peaks.get("hbm_gbs"),
             "unit": "GB/s",
             "frac": apply_bytes / (apply_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-            "traffic": None,
+            "traffic": traffic.get("k_apply_per_launch"),
+            "traffic_unit": f"DRAM bytes per launch, ncu ({traffic.get('file')})",
             "algorithmic_bytes": apply_bytes,
             "note": "bytes = nnz*12 + nt*4 + ns*C*8 + nt*C*8 (SURVEY §8(d)); peak of measured"
                     if not peaks.get("fallback") else "peak of fallback",
