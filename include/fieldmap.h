@@ -281,6 +281,25 @@ int fm_apply(int64_t nrows, const int64_t *row_off, const int32_t *col, const do
              const int32_t *row_target, const double *X, int32_t ncomp, double *Y,
              fm_stream_t stream);
 
+/* ------------------------------- f1: element point localization (next)
+ * locate_batch (_ext.pyx:88-152; caller locate_arrays, locate.py:175-186):
+ * per query point (n, 2), the first element -- in the stored order of its
+ * cell of the element grid (the reference UniformGrid's CSR, row-major
+ * cells iy*nx + ix) -- whose tol-halo contains it, barycentric coordinates
+ * and its classification on the lowest-dimensional mesh entity within
+ * tolerance: dim 0 (vertex gid), 1 (edge id), 2 (element gid).  Mesh arrays
+ * as the reference's Mesh: tri_xy (ne, 3, 2), tri_verts/tri_edges (ne, 3),
+ * vert_gid (nv), tri_gid (ne), inv2a (ne), epsfac (ne, 3).  Outputs (all n):
+ * found u8, elem/dim/ent int64 (-1 when not found), bary (n, 3) f64 (NaN when
+ * not found).  Bitwise equal to the reference. */
+int fm_locate_batch(const double *points, int64_t n, const double *tri_xy,
+                    const int64_t *tri_verts, const int64_t *tri_edges, const int64_t *vert_gid,
+                    const int64_t *tri_gid, const double *inv2a, const double *epsfac, double gx0,
+                    double gy0, double gdx, double gdy, int64_t nx, int64_t ny,
+                    const int64_t *cell_off, const int64_t *cell_items, double tol,
+                    uint8_t *found, int64_t *elem, int64_t *dim, int64_t *ent, double *bary,
+                    fm_stream_t stream);
+
 /* ---------------------------------------------------- measurement
  * FP64 FMA-chain peak probe (the build kernel's roofline denominator; the
  * driver's MEASURED_PEAKS.json has no FP64 figure).  Runs `iters` dependent

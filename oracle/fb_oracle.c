@@ -474,3 +474,55 @@ int orc_fit_many(int dim, int degree, double lam, int centering, const double *t
     }
     return 0;
 }
+
+/* ------------------------------------------------------------ locate_batch
+ * _ext.pyx:88-152: per point, its cell of the element grid (row-major
+ * iy*nx+ix), the cell's candidate elements in stored (ascending id) order,
+ * barycentric coordinates with the reference's operation order, first
+ * element whose tol-halo contains the point; classification on the lowest
+ * dimensional entity within tolerance (2 small -> vertex, 1 -> edge, else
+ * element).  Outputs pre-filled by the caller (found 0, ids -1, bary NaN). */
+void orc_locate_batch(const double *points, int64_t n, const double *tri_xy,
+                      const int64_t *tri_verts, const int64_t *tri_edges,
+                      const int64_t *vert_gid, const int64_t *tri_gid, const double *inv2a,
+                      const double *epsfac, double gx0, double gy0, double gdx, double gdy,
+                      int64_t nx, int64_t ny, const int64_t *cell_off,
+                      const int64_t *cell_items, double tol, uint8_t *found, int64_t *elem,
+                      int64_t *dim, int64_t *ent, double *bary) {
+    const double inv_dx = 1.0 / gdx, inv_dy = 1.0 / gdy;
+    for (int64_t i = 0; i < n; i++) {
+        const double px = points[2 * i], py = points[2 * i + 1];
+        const int64_t c = cell_of(py, gy0, inv_dy, ny) * nx + cell_of(px, gx0, inv_dx, nx);
+        for (int64_t j = cell_off[c]; j < cell_off[c + 1]; j++) {
+            const int64_t t = cell_items[j];
+            const double *P = tri_xy + 6 * t;
+            const double b0 = ((P[2] - px) * (P[5] - py) - (P[3] - py) * (P[4] - px)) * inv2a[t];
+            const double b1 = ((P[4] - px) * (P[1] - py) - (P[5] - py) * (P[0] - px)) * inv2a[t];
+            const double b2 = 1.0 - b0 - b1;
+            const double e0 = tol * epsfac[3 * t], e1 = tol * epsfac[3 * t + 1],
+                         e2 = tol * epsfac[3 * t + 2];
+            if (b0 >= -e0 && b1 >= -e1 && b2 >= -e2) {
+                found[i] = 1;
+                elem[i] = t;
+                bary[3 * i] = b0;
+                bary[3 * i + 1] = b1;
+                bary[3 * i + 2] = b2;
+                const int s0 = b0 <= e0, s1 = b1 <= e1, s2 = b2 <= e2;
+                const int nsmall = s0 + s1 + s2;
+                if (nsmall == 2) {
+                    const int v = !s0 ? 0 : (!s1 ? 1 : 2);
+                    dim[i] = 0;
+                    ent[i] = vert_gid[tri_verts[3 * t + v]];
+                } else if (nsmall == 1) {
+                    const int k = s0 ? 0 : (s1 ? 1 : 2);
+                    dim[i] = 1;
+                    ent[i] = tri_edges[3 * t + k];
+                } else {
+                    dim[i] = 2;
+                    ent[i] = tri_gid[t];
+                }
+                break;
+            }
+        }
+    }
+}

@@ -270,3 +270,26 @@ def transfer(src, vals, targets, degree, kind, a, selection, lam=0.0, centering=
     values, _c, status = fit_many_nd(targets, off, idx, w, src, vals, degree, lam,
                                      centering, nthreads)
     return values, status, (off, idx, dist, w)
+
+
+def locate_batch(points, tri_xy, tri_verts, tri_edges, vert_gid, tri_gid, inv2a, epsfac,
+                 gx0, gy0, gdx, gdy, nx, ny, cell_off, cell_items, tol):
+    """_ext.pyx:88-152 (same signature and outputs as the reference)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    n = pts.shape[0]
+    found = np.zeros(n, dtype=np.uint8)
+    elem = np.full(n, -1, dtype=np.int64)
+    dim = np.full(n, -1, dtype=np.int64)
+    ent = np.full(n, -1, dtype=np.int64)
+    bary = np.full((n, 3), np.nan, dtype=np.float64)
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+    a = [f64(tri_xy), i64(tri_verts), i64(tri_edges), i64(vert_gid), i64(tri_gid), f64(inv2a),
+         f64(epsfac), i64(cell_off), i64(cell_items)]
+    L = lib()
+    L.orc_locate_batch(_p(pts), ctypes.c_int64(n), _p(a[0]), _p(a[1]), _p(a[2]), _p(a[3]),
+                       _p(a[4]), _p(a[5]), _p(a[6]), ctypes.c_double(gx0), ctypes.c_double(gy0),
+                       ctypes.c_double(gdx), ctypes.c_double(gdy), ctypes.c_int64(nx),
+                       ctypes.c_int64(ny), _p(a[7]), _p(a[8]), ctypes.c_double(tol), _p(found),
+                       _p(elem), _p(dim), _p(ent), _p(bary))
+    return found.astype(bool), elem, dim, ent, bary

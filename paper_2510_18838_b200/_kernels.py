@@ -14,8 +14,9 @@ numpy out, device in between.  A maintainer can therefore do
 
 and the reference's pointwise/locate code (which resolves `_kernels.<fn>`
 at call time, pointwise.py:17, 240, 256, 302) runs on the GPU (see
-INTEGRATION.md).  `locate_batch` and `clip_batch` are not part of this path
-(OUT).
+INTEGRATION.md).  `locate_batch` (element localization, the seam's other
+search export) is here too, bitwise equal to
+_ext.pyx:88-152; `clip_batch` (conservative transfer) is OUT.
 
 fixed/adaptive_radius_supports receive the caller's grid geometry and use
 it for the device grid; the caller's host CSR (cell_off, cell_items) is not
@@ -112,3 +113,33 @@ def fit_many(targets, sup_off, sup_idx, sup_w, src_xy, src_val, degree, lam, cen
         D.to_device(np.ascontiguousarray(src_val, dtype=np.float64)), int(degree), float(lam),
         bool(centering), max_m)
     return values.cpu().numpy(), coeffs.cpu().numpy(), status.cpu().numpy()
+
+
+def locate_batch(points, tri_xy, tri_verts, tri_edges, vert_gid, tri_gid, inv2a, epsfac,
+                 gx0, gy0, gdx, gdy, nx, ny, cell_off, cell_items, tol):
+    """Grid-accelerated point localization with entity classification
+    (_ext.pyx:88-152): (found bool, elem, dim, ent int64, bary (n, 3) f64)."""
+    from . import _lib as L
+
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    n = pts.shape[0]
+    if n == 0:
+        return (np.zeros(0, dtype=bool), np.full(0, -1, np.int64), np.full(0, -1, np.int64),
+                np.full(0, -1, np.int64), np.full((0, 3), np.nan))
+    f64 = lambda a: D.to_device(np.ascontiguousarray(a, dtype=np.float64))  # noqa: E731
+    i64 = lambda a: torch.from_numpy(  # noqa: E731
+        np.ascontiguousarray(a, dtype=np.int64)).to(D._dev())
+    dev = [f64(pts), f64(tri_xy), i64(tri_verts), i64(tri_edges), i64(vert_gid), i64(tri_gid),
+           f64(inv2a), f64(epsfac), i64(cell_off), i64(cell_items)]
+    found = torch.empty(n, dtype=torch.uint8, device=dev[0].device)
+    elem = torch.empty(n, dtype=torch.int64, device=dev[0].device)
+    dim = torch.empty_like(elem)
+    ent = torch.empty_like(elem)
+    bary = torch.empty((n, 3), dtype=torch.float64, device=dev[0].device)
+    P = L.ptr
+    L.check(L.lib().fm_locate_batch(P(dev[0]), n, *[P(a) for a in dev[1:8]], float(gx0),
+                                    float(gy0), float(gdx), float(gdy), int(nx), int(ny),
+                                    P(dev[8]), P(dev[9]), float(tol), P(found), P(elem), P(dim),
+                                    P(ent), P(bary), D._stream()), "fm_locate_batch")
+    return (found.cpu().numpy().astype(bool), elem.cpu().numpy(), dim.cpu().numpy(),
+            ent.cpu().numpy(), bary.cpu().numpy())

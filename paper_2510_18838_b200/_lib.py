@@ -23,6 +23,7 @@ FM_BUCKET_EDGES = (8, 16, 24, 32, 48, 64, 96, 128, 2147483647)
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
+c_f64 = ctypes.c_double
 c_dbl = ctypes.c_double
 c_vp = ctypes.c_void_p
 c_sz = ctypes.c_size_t
@@ -88,6 +89,9 @@ SIGNATURES = {
                                    c_vp, c_vp]),
     "fm_apply": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
     "fm_fp64_probe": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "fm_locate_batch": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64,
+                                c_f64, c_f64, c_f64, c_i64, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp,
+                                c_vp, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

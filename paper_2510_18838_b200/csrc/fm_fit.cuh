@@ -153,13 +153,15 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     static_for<0, K>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         const double x0 = __shfl_sync(FM_FULL_MASK, A[j / G][j], gbase + (j % G));
+        // reflector entries of this lane's rows: 0 above the pivot, v_j on it,
+        // A[i][j] below -- selected once per column, so the dot products and
+        // updates below are unconditional (a zero entry is an exact no-op)
+        double v[ROWS];
+#pragma unroll
+        for (int q = 0; q < ROWS; q++) v[q] = row_below<G>(q, j, glane) ? A[q][j] : 0.0;
         double sl = 0.0;
 #pragma unroll
-        for (int q = 0; q < ROWS; q++) {
-            const int i = q * G + glane;
-            if (row_below<G>(q, j, glane)) sl = fma(A[q][j], A[q][j], sl);
-            (void)i;
-        }
+        for (int q = 0; q < ROWS; q++) sl = fma(v[q], v[q], sl);
         const double sigma = group_sum<G>(sl);
         double gj, bj, vj, ib;
         if (sigma == 0.0) {
@@ -181,17 +183,15 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
             sIb[j] = ib;
             sV0[j] = vj;
         }
+#pragma unroll
+        for (int q = 0; q < ROWS; q++)
+            if (row_diag<G>(q, j, glane)) v[q] = vj;
         double dot[NC];
 #pragma unroll
         for (int l = j + 1; l < NC; l++) {
             double pl = 0.0;
 #pragma unroll
-            for (int q = 0; q < ROWS; q++) {
-                const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) pl = fma(vj, A[q][l], pl);
-                else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], A[q][l], pl);
-                (void)i;
-            }
+            for (int q = 0; q < ROWS; q++) pl = fma(v[q], A[q][l], pl);
             dot[l] = pl;
         }
 #pragma unroll
@@ -200,12 +200,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         for (int l = j + 1; l < NC; l++) {
             const double td = gj * dot[l];
 #pragma unroll
-            for (int q = 0; q < ROWS; q++) {
-                const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) A[q][l] = fma(-td, vj, A[q][l]);
-                else if (row_below<G>(q, j, glane)) A[q][l] = fma(-td, A[q][j], A[q][l]);
-                (void)i;
-            }
+            for (int q = 0; q < ROWS; q++) A[q][l] = fma(-td, v[q], A[q][l]);
         }
 #pragma unroll
         for (int q = 0; q < ROWS; q++)
@@ -329,22 +324,16 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         static_for<0, K>([&](auto jj) {
             constexpr int j = K - 1 - decltype(jj)::value;
             const double vj = sV0[j];
+            double v[ROWS];
+#pragma unroll
+            for (int q = 0; q < ROWS; q++)
+                v[q] = row_diag<G>(q, j, glane) ? vj : row_below<G>(q, j, glane) ? A[q][j] : 0.0;
             double pl = 0.0;
 #pragma unroll
-            for (int q = 0; q < ROWS; q++) {
-                const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) pl = fma(vj, yy[q], pl);
-                else if (row_below<G>(q, j, glane)) pl = fma(A[q][j], yy[q], pl);
-                (void)i;
-            }
+            for (int q = 0; q < ROWS; q++) pl = fma(v[q], yy[q], pl);
             const double td = sGam[j] * group_sum<G>(pl);
 #pragma unroll
-            for (int q = 0; q < ROWS; q++) {
-                const int i = q * G + glane;
-                if (row_diag<G>(q, j, glane)) yy[q] = fma(-td, vj, yy[q]);
-                else if (row_below<G>(q, j, glane)) yy[q] = fma(-td, A[q][j], yy[q]);
-                (void)i;
-            }
+            for (int q = 0; q < ROWS; q++) yy[q] = fma(-td, v[q], yy[q]);
         });
 #pragma unroll
         for (int q = 0; q < ROWS; q++) y[q] = valid[q] ? w[q] * yy[q] : 0.0;

@@ -429,7 +429,10 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
 // rebuilt by the rescan build.
 // stats[8]: max, min, #short, first short, #status, first status, #overflow, 0.
 template <int DIM, int G>
-__global__ void __launch_bounds__(kBlock) k_select(SearchArgs s, int32_t min_required, int lcap,
+#ifndef FM_SELECT_MINB
+#define FM_SELECT_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlock, FM_SELECT_MINB) k_select(SearchArgs s, int32_t min_required, int lcap,
                                                    int32_t *__restrict__ counts,
                                                    double *__restrict__ radii,
                                                    uint8_t *__restrict__ status,
@@ -662,7 +665,10 @@ int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *i
     return FM_OK;
 }
 
-constexpr int kSelectListCap = 128;  // per-group candidate list of the select pass
+#ifndef FM_SELECT_LCAP
+#define FM_SELECT_LCAP 128
+#endif
+constexpr int kSelectListCap = FM_SELECT_LCAP;  // per-group candidate list of the select pass
 
 template <int DIM>
 int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,

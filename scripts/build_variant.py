@@ -1,6 +1,9 @@
 """Build an experimental variant of libfieldmap.so with extra -D flags.
 
-    python scripts/build_variant.py NAME -DFOO=1 ...
+    python scripts/build_variant.py NAME [--only fm_d2,fm_api] -DFOO=1 ...
+
+--only recompiles just those translation units and links them with the
+in-tree build's objects for the rest (a full variant build takes minutes).
 
 Output: paper_2510_18838_b200/_lib/var/libfieldmap_NAME.so; load it with
 FM_LIB_PATH=<that path> (A/B timing on the GPU box in one gpurun call).
@@ -17,6 +20,10 @@ from paper_2510_18838_b200 import _build as B  # noqa: E402
 
 def main():
     name, extra = sys.argv[1], sys.argv[2:]
+    only = None
+    if extra[:1] == ["--only"]:
+        only = set(extra[1].split(","))
+        extra = extra[2:]
     obj_dir = os.path.join(B.ROOT, "build", "var_" + name)
     out_dir = os.path.join(B.LIBDIR, "var")
     os.makedirs(obj_dir, exist_ok=True)
@@ -29,11 +36,13 @@ def main():
                               stderr=subprocess.DEVNULL)
         return obj
 
-    with cf.ThreadPoolExecutor(len(srcs)) as ex:
-        objs = list(ex.map(one, srcs))
+    todo = [x for x in srcs if only is None or os.path.basename(x)[:-3] in only]
+    with cf.ThreadPoolExecutor(max(1, len(todo))) as ex:
+        built = dict(zip(todo, ex.map(one, todo)))
+    objs = [built.get(x) or os.path.join(B.OBJ, os.path.basename(x)[:-3] + ".o") for x in srcs]
     lib = os.path.join(out_dir, f"libfieldmap_{name}.so")
     subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"])
-    for o in objs:
+    for o in built.values():
         os.remove(o)
     print(lib)
 

@@ -200,7 +200,43 @@ def fit_local_cases():
     save("fit_local", **out)
 
 
+def locate_cases():
+    """locate_batch (_ext.pyx:88-152) on two meshes with the reference's own
+    UniformGrid: interior points, vertices (dim 0), edge midpoints (dim 1),
+    centroids (dim 2), points just outside (tol halo) and far outside."""
+    out = {}
+    for name, m in (("sq", fb.square(12)), ("disk", fb.disk(1.0, 6))):
+        g = fb.build_grid(m)
+        rng = np.random.RandomState(7)
+        lo, hi = m.bbox[0], m.bbox[1]
+        span = hi - lo
+        e = m.edges
+        mids = 0.5 * (m.coords[e[:, 0]] + m.coords[e[:, 1]])
+        pts = np.concatenate([
+            rng.uniform(lo - 0.1 * span, hi + 0.1 * span, (400, 2)),
+            m.coords, mids, m.centroids(),
+            m.coords + 1e-12 * rng.standard_normal(m.coords.shape),
+            mids + 3e-11 * rng.standard_normal(mids.shape),
+        ])
+        pts = np.ascontiguousarray(pts)
+        for tol in (1e-10, 0.0, 1e-6):
+            res = K.locate_batch(pts, m.tri_xy, m.tris, m.tri_edges, m.vert_gid, m.tri_gid,
+                                 m.inv2a, m.epsfac, float(g.lo[0]), float(g.lo[1]), g.dx, g.dy,
+                                 g.nx, g.ny, g.cell_offsets, g.cell_items, tol)
+            for k, a in zip(("found", "elem", "dim", "ent", "bary"), res):
+                out[f"{name}_{tol:g}_{k}"] = a
+        out.update({f"{name}_pts": pts, f"{name}_tri_xy": m.tri_xy, f"{name}_tris": m.tris,
+                    f"{name}_tri_edges": m.tri_edges, f"{name}_vert_gid": m.vert_gid,
+                    f"{name}_tri_gid": m.tri_gid, f"{name}_inv2a": m.inv2a,
+                    f"{name}_epsfac": m.epsfac,
+                    f"{name}_grid": np.array([g.lo[0], g.lo[1], g.dx, g.dy]),
+                    f"{name}_grid_n": np.array([g.nx, g.ny]),
+                    f"{name}_cell_off": g.cell_offsets, f"{name}_cell_items": g.cell_items})
+    save("locate", **out)
+
+
 if __name__ == "__main__":
+    locate_cases()
     rbf_table()
     disk_small()
     c1()

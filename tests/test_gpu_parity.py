@@ -582,3 +582,37 @@ def test_fit_point_cloud_tensor_paths():
     empty = P.fit_point_cloud(torch.from_numpy(src), torch.from_numpy(V),
                               torch.zeros((0, 2), dtype=torch.float64), spec)
     assert tuple(empty.shape) == (0, 8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["sq", "disk"])
+@pytest.mark.parametrize("tol", [1e-10, 0.0, 1e-6])
+def test_locate_batch_bitwise(name, tol):
+    """fm_locate_batch vs the reference's own locate_batch outputs
+    (_ext.pyx:88-152, golden fixture): found/elem/dim/ent/bary bitwise."""
+    d = golden("locate")
+    g, gn = d[f"{name}_grid"], d[f"{name}_grid_n"]
+    got = Kb.locate_batch(d[f"{name}_pts"], d[f"{name}_tri_xy"], d[f"{name}_tris"],
+                          d[f"{name}_tri_edges"], d[f"{name}_vert_gid"], d[f"{name}_tri_gid"],
+                          d[f"{name}_inv2a"], d[f"{name}_epsfac"], float(g[0]), float(g[1]),
+                          float(g[2]), float(g[3]), int(gn[0]), int(gn[1]),
+                          d[f"{name}_cell_off"], d[f"{name}_cell_items"], tol)
+    for k, a in zip(("found", "elem", "dim", "ent", "bary"), got):
+        want = d[f"{name}_{tol:g}_{k}"]
+        assert a.dtype == want.dtype and a.shape == want.shape, k
+        assert np.array_equal(a, want, equal_nan=(k == "bary")), k
+
+
+@pytest.mark.gpu
+def test_locate_batch_large_vs_oracle():
+    """100k random points (some outside) on the golden square mesh: GPU == C oracle."""
+    d = golden("locate")
+    sys_pts = np.random.default_rng(3).uniform(-0.05, 1.05, (100000, 2))
+    g, gn = d["sq_grid"], d["sq_grid_n"]
+    args = (d["sq_tri_xy"], d["sq_tris"], d["sq_tri_edges"], d["sq_vert_gid"], d["sq_tri_gid"],
+            d["sq_inv2a"], d["sq_epsfac"], float(g[0]), float(g[1]), float(g[2]), float(g[3]),
+            int(gn[0]), int(gn[1]), d["sq_cell_off"], d["sq_cell_items"], 1e-10)
+    got = Kb.locate_batch(sys_pts, *args)
+    want = O.locate_batch(sys_pts, *args)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b, equal_nan=True)

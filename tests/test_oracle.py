@@ -173,3 +173,24 @@ def test_oracle_equals_reference_ext_adaptive_fit():
         b = E.fit_many(tg, off, idx, w, src, vals, deg, 0.0, True)
         for x, y in zip(a, b):
             assert np.array_equal(x, y, equal_nan=True)
+
+
+def _locate_case(d, name, tol, fn):
+    g = d[f"{name}_grid"]
+    gn = d[f"{name}_grid_n"]
+    return fn(d[f"{name}_pts"], d[f"{name}_tri_xy"], d[f"{name}_tris"], d[f"{name}_tri_edges"],
+              d[f"{name}_vert_gid"], d[f"{name}_tri_gid"], d[f"{name}_inv2a"],
+              d[f"{name}_epsfac"], float(g[0]), float(g[1]), float(g[2]), float(g[3]),
+              int(gn[0]), int(gn[1]), d[f"{name}_cell_off"], d[f"{name}_cell_items"], tol)
+
+
+@pytest.mark.parametrize("name", ["sq", "disk"])
+@pytest.mark.parametrize("tol", [1e-10, 0.0, 1e-6])
+def test_oracle_locate_batch_bitwise(name, tol):
+    """locate_batch restatement vs the reference's own outputs (_ext.pyx:88-152)."""
+    d = golden("locate")
+    got = _locate_case(d, name, tol, O.locate_batch)
+    for k, a in zip(("found", "elem", "dim", "ent", "bary"), got):
+        want = d[f"{name}_{tol:g}_{k}"]
+        assert a.dtype == want.dtype
+        assert np.array_equal(a, want, equal_nan=(k == "bary")), k
