@@ -334,8 +334,13 @@ def run_b200(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        e2e_steps = []
         for _ in range(args.steps):
+            ts = time.perf_counter()
             Yh = e2e_step()
+            e2e_steps.append(1e3 * (time.perf_counter() - ts))
+        if os.environ.get("FM_E2E_DEBUG"):
+            print("e2e per-step ms:", " ".join(f"{x:.2f}" for x in e2e_steps), file=sys.stderr)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
