@@ -616,3 +616,28 @@ def test_locate_batch_large_vs_oracle():
     want = O.locate_batch(sys_pts, *args)
     for a, b in zip(got, want):
         assert np.array_equal(a, b, equal_nan=True)
+
+
+@pytest.mark.gpu
+def test_prepared_transfer_all_size_buckets_and_overflow():
+    """Clustered sources + a fixed radius: support sizes 6 .. 143, so the
+    build runs one fit shape per size bucket (<= 8 ... > 128) and the
+    supports beyond the 64-entry slots go through the overflow rescan; the
+    operator applied to 3 components matches the CPU oracle per column."""
+    rng = np.random.default_rng(21)
+    bg = rng.uniform(0, 1, (6000, 2))
+    cl = np.clip(0.5 + 0.03 * rng.standard_normal((250, 2)), 0, 1)
+    src = np.concatenate([bg, cl])
+    tg = rng.uniform(0.05, 0.95, (2000, 2))
+    V = synth.sincos_field(src, 3)
+    r = 0.035
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4), P.FixedRadius(r))
+    pt = P.PreparedTransfer(src, tg, spec)
+    Y = pt.apply(V)
+    want, st, (off, _idx, _d, _w) = O.transfer(src, V, tg, 2, O.RBF_C4, 2.0, ("fixed", r))
+    counts = np.diff(off)
+    edges = [8, 16, 24, 32, 48, 64, 96, 128]
+    assert counts.max() > 128 and counts.min() <= 8
+    assert all(np.any((counts > lo) & (counts <= hi)) for lo, hi in zip(edges[:-1], edges[1:]))
+    assert (st == 0).all()
+    assert _rel(Y, want) < VALUE_RTOL
