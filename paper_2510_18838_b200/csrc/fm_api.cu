@@ -25,8 +25,13 @@ __global__ void k_rbf(int kind, double a, double r_c, const double *__restrict__
 // the X rows -- one 16-byte load per lane per nonzero, 8 in flight.
 constexpr int kApplyChunk = 256;  // staged nonzeros per warp and pass
 
+#ifdef FM_APPLY_MINB
+#define FM_APPLY_BOUNDS __launch_bounds__(256, FM_APPLY_MINB)
+#else
+#define FM_APPLY_BOUNDS __launch_bounds__(256)
+#endif
 template <int L, int V>
-__global__ void __launch_bounds__(256) k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
+__global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
                                                const int32_t *__restrict__ col,
                                                const double *__restrict__ val,
                                                const int32_t *__restrict__ row_target,
@@ -34,7 +39,10 @@ __global__ void __launch_bounds__(256) k_apply(int64_t nrows, const int64_t *__r
                                                double *__restrict__ Y) {
     constexpr int C = L * V;
     constexpr int RPW = 32 / L;
-    constexpr int U = 8;
+#ifndef FM_APPLY_U
+#define FM_APPLY_U 8
+#endif
+    constexpr int U = FM_APPLY_U;
     __shared__ int32_t s_col[8][kApplyChunk];
     __shared__ double s_val[8][kApplyChunk];
     const int wib = threadIdx.x >> 5;
