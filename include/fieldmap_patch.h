@@ -1,0 +1,44 @@
+/* fieldmap_patch.h -- element-patch support selection.
+ *
+ * Replaces the per-target Python BFS of the reference's ElementPatch branch:
+ * `_PatchTopology.neighbors` / `patch_dofs` (pointwise.py:190-230) as called
+ * from `_select_batch` (pointwise.py:271-296).  Same conventions as
+ * fieldmap.h: device pointers, sizes and a stream; FM_OK or a negative
+ * FM_ERR_* code; no global state.
+ */
+#ifndef FIELDMAP_PATCH_H
+#define FIELDMAP_PATCH_H
+
+#include "fieldmap.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Largest patch one target can hold: elements reached within `layers`
+ * edge-adjacency hops, and distinct vertex dofs of those elements.  A larger
+ * patch reports count -1 for that target (Python: FieldmapError). */
+#define FM_PATCH_MAX_ELEMS 128
+#define FM_PATCH_MAX_DOFS 256
+
+/* Per target i with containing element seed[i] (locate_batch's `elem`,
+ * int64, >= 0): the elements within `layers` hops over the element
+ * adjacency CSR (adj_off int64 (ne+1), adj int64 -- each interior edge
+ * contributes both directions, pointwise.py:195-200), sorted ascending
+ * (pointwise.py:226); dofs = those element ids when `centroids` != 0, else
+ * the sorted distinct vertex ids of tris[elems] (tris int64 (ne, 3),
+ * pointwise.py:229).
+ *   fm_patch_count: counts int64 (nt) (-1 on overflow).
+ *   fm_patch_fill:  idx int64 at off[i] .. off[i+1] (off = exclusive scan of
+ *                   counts, int64 (nt+1)).  Bitwise equal to the reference. */
+int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *adj_off, const int64_t *adj,
+                   const int64_t *tris, int64_t ne, int32_t layers, int32_t centroids,
+                   int64_t *counts, fm_stream_t stream);
+int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *adj_off, const int64_t *adj,
+                  const int64_t *tris, int64_t ne, int32_t layers, int32_t centroids,
+                  const int64_t *off, int64_t *idx, fm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIELDMAP_PATCH_H */

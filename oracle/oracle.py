@@ -293,3 +293,37 @@ def locate_batch(points, tri_xy, tri_verts, tri_edges, vert_gid, tri_gid, inv2a,
                        ctypes.c_int64(ny), _p(a[7]), _p(a[8]), ctypes.c_double(tol), _p(found),
                        _p(elem), _p(dim), _p(ent), _p(bary))
     return found.astype(bool), elem, dim, ent, bary
+
+
+def patch_supports(seed, edge_tris, tris, layers, centroids):
+    """Element-patch supports (pointwise.py:190-230, _select_batch's patch
+    branch 271-296): per seed element, the elements within `layers` hops over
+    interior-edge adjacency (both directions, 195-200), sorted (226); dofs are
+    those elements (centroids) or np.unique of their vertices (229).  Plain
+    Python BFS -- small cases only.  Returns (offsets int64 (nt+1), idx int64)."""
+    et = np.asarray(edge_tris, dtype=np.int64)
+    interior = et[:, 1] >= 0
+    nbrs = {}
+    for a, b in zip(et[interior, 0].tolist(), et[interior, 1].tolist()):
+        nbrs.setdefault(a, []).append(b)
+        nbrs.setdefault(b, []).append(a)
+    tris = np.asarray(tris, dtype=np.int64)
+    off = [0]
+    parts = []
+    for s in np.asarray(seed, dtype=np.int64).tolist():
+        seen = {s}
+        frontier = [s]
+        for _ in range(layers):
+            nxt = []
+            for t in frontier:
+                for nb in nbrs.get(t, ()):
+                    if nb not in seen:
+                        seen.add(nb)
+                        nxt.append(nb)
+            frontier = nxt
+        elems = np.array(sorted(seen), dtype=np.int64)
+        dofs = elems if centroids else np.unique(tris[elems].reshape(-1))
+        parts.append(dofs)
+        off.append(off[-1] + dofs.size)
+    idx = np.concatenate(parts) if parts else np.empty(0, np.int64)
+    return np.array(off, dtype=np.int64), idx.astype(np.int64)

@@ -143,3 +143,23 @@ def locate_batch(points, tri_xy, tri_verts, tri_edges, vert_gid, tri_gid, inv2a,
                                     P(ent), P(bary), D._stream()), "fm_locate_batch")
     return (found.cpu().numpy().astype(bool), elem.cpu().numpy(), dim.cpu().numpy(),
             ent.cpu().numpy(), bary.cpu().numpy())
+
+
+def patch_supports(seed, tris, edge_tris, layers, centroids):
+    """ElementPatch support CSR for seed elements (the loop of _select_batch's
+    patch branch over _PatchTopology.patch_dofs, pointwise.py:212-230,
+    286-296): (offsets int64 (nt+1), idx int64, counts int64 (nt)), computed
+    by fm_patch_count / fm_patch_fill.  A patch larger than the kernel's
+    per-target bound raises FieldmapError."""
+    from ._lib import FieldmapError
+
+    topo = D.PatchTopology.from_mesh_arrays(np.ascontiguousarray(tris, dtype=np.int64),
+                                            np.ascontiguousarray(edge_tris, dtype=np.int64))
+    off, idx, counts = D.patch_supports(topo, np.ascontiguousarray(seed, dtype=np.int64),
+                                        layers, centroids)
+    counts = counts.cpu().numpy()
+    if (counts < 0).any():
+        i = int(np.argmax(counts < 0))
+        raise FieldmapError(f"element patch of target {i} exceeds the kernel's per-target "
+                            "bound (FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)")
+    return off.cpu().numpy(), idx.cpu().numpy(), counts

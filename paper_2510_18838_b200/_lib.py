@@ -56,7 +56,7 @@ class FmLists(ctypes.Structure):
 
 
 P = ctypes.POINTER
-# name -> (restype, argtypes); mirrors include/fieldmap.h
+# name -> (restype, argtypes); mirrors include/fieldmap.h and fieldmap_patch.h
 SIGNATURES = {
     "fm_version": (c_i32, []),
     "fm_error_string": (ctypes.c_char_p, [c_i32]),
@@ -89,6 +89,10 @@ SIGNATURES = {
                                    c_vp, c_vp]),
     "fm_apply": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
     "fm_fp64_probe": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp]),
+    # include/fieldmap_patch.h
+    "fm_patch_count": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]),
+    "fm_patch_fill": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp,
+                              c_vp]),
     "fm_locate_batch": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64,
                                 c_f64, c_f64, c_f64, c_i64, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp,
                                 c_vp, c_vp, c_vp, c_vp]),

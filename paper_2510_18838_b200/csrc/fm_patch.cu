@@ -1,0 +1,143 @@
+// fm_patch.cu -- element-patch support selection:
+// the reference's per-target Python BFS (_PatchTopology.patch_dofs,
+// pointwise.py:212-230) as one thread per target.
+//
+// The patch is the set of elements within `layers` hops of the seed element,
+// so the BFS visiting order does not matter: each thread grows its element
+// list layer by layer (frontier = the elements appended in the previous
+// layer, membership by a linear scan of the short list), sorts it, and either
+// emits it (centroid dofs) or merges the elements' three vertices into a
+// sorted, de-duplicated list (vertex dofs, np.unique of pointwise.py:229).
+// The lists live in per-thread local memory (L1-resident: a 1-layer patch is
+// ~13 elements / ~12 vertices); the work is a short dependent scan, latency
+// bound, so the grid is sized for many resident warps.  Two passes (count,
+// then fill at the scanned offsets) recompute the patch instead of staging
+// it, which keeps the output exactly nnz long.
+#include <algorithm>
+
+#include "../../include/fieldmap_patch.h"
+#include "fm_common.cuh"
+
+namespace fm {
+
+template <bool FILL>
+__global__ void __launch_bounds__(128)
+    k_patch(const int64_t *__restrict__ seed, int64_t nt, const int64_t *__restrict__ adj_off,
+            const int64_t *__restrict__ adj, const int64_t *__restrict__ tris, int32_t layers,
+            int32_t centroids, int64_t *__restrict__ counts, const int64_t *__restrict__ off,
+            int64_t *__restrict__ idx) {
+    int32_t el[FM_PATCH_MAX_ELEMS];
+    int32_t dof[FM_PATCH_MAX_DOFS];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int n = 1;
+        bool overflow = false;
+        el[0] = (int32_t)seed[i];
+        int fs = 0, fe = 1;  // frontier [fs, fe)
+        for (int layer = 0; layer < layers && !overflow && fs < fe; layer++) {
+            for (int f = fs; f < fe && !overflow; f++) {
+                const int32_t t = el[f];
+                const int64_t a1 = __ldg(adj_off + t + 1);
+                for (int64_t a = __ldg(adj_off + t); a < a1; a++) {
+                    const int32_t nb = (int32_t)__ldg(adj + a);
+                    bool seen = false;
+                    for (int q = 0; q < n; q++) seen |= (el[q] == nb);
+                    if (seen) continue;
+                    if (n == FM_PATCH_MAX_ELEMS) {
+                        overflow = true;
+                        break;
+                    }
+                    el[n++] = nb;
+                }
+            }
+            fs = fe;
+            fe = n;
+        }
+        if (overflow) {
+            if (!FILL) counts[i] = -1;
+            continue;
+        }
+        // sorted(seen) (pointwise.py:226): insertion sort of a short list
+        for (int a = 1; a < n; a++) {
+            const int32_t v = el[a];
+            int b = a - 1;
+            while (b >= 0 && el[b] > v) {
+                el[b + 1] = el[b];
+                b--;
+            }
+            el[b + 1] = v;
+        }
+        if (centroids) {
+            if (FILL) {
+                int64_t *o = idx + off[i];
+                for (int a = 0; a < n; a++) o[a] = el[a];
+            } else {
+                counts[i] = n;
+            }
+            continue;
+        }
+        // np.unique(tris[elems]) (pointwise.py:229): sorted insert with dedup
+        int m = 0;
+        for (int a = 0; a < n && !overflow; a++) {
+            const int64_t *tv = tris + 3 * (int64_t)el[a];
+            for (int c = 0; c < 3; c++) {
+                const int32_t v = (int32_t)__ldg(tv + c);
+                int b = m - 1;
+                while (b >= 0 && dof[b] > v) b--;
+                if (b >= 0 && dof[b] == v) continue;
+                if (m == FM_PATCH_MAX_DOFS) {
+                    overflow = true;
+                    break;
+                }
+                for (int q = m; q > b + 1; q--) dof[q] = dof[q - 1];
+                dof[b + 1] = v;
+                m++;
+            }
+        }
+        if (FILL) {
+            if (!overflow) {
+                int64_t *o = idx + off[i];
+                for (int a = 0; a < m; a++) o[a] = dof[a];
+            }
+        } else {
+            counts[i] = overflow ? -1 : m;
+        }
+    }
+}
+
+static int launch_patch(bool fill, const int64_t *seed, int64_t nt, const int64_t *adj_off,
+                        const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
+                        int32_t centroids, int64_t *counts, const int64_t *off, int64_t *idx,
+                        cudaStream_t stream) {
+    if (nt < 0 || ne < 1 || layers < 1 || ne > INT32_MAX) return FM_ERR_ARG;
+    if (nt == 0) return FM_OK;
+    if (!seed || !adj_off || !adj || (!centroids && !tris)) return FM_ERR_ARG;
+    if (fill ? (!off || !idx) : !counts) return FM_ERR_ARG;
+    const int threads = 128;
+    const int blocks = (int)std::min<int64_t>((nt + threads - 1) / threads, (int64_t)kSMs * 16);
+    if (fill)
+        k_patch<true><<<blocks, threads, 0, stream>>>(seed, nt, adj_off, adj, tris, layers,
+                                                      centroids, nullptr, off, idx);
+    else
+        k_patch<false><<<blocks, threads, 0, stream>>>(seed, nt, adj_off, adj, tris, layers,
+                                                       centroids, counts, nullptr, nullptr);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+}  // namespace fm
+
+extern "C" int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *adj_off,
+                              const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
+                              int32_t centroids, int64_t *counts, fm_stream_t stream) {
+    return fm::launch_patch(false, seed, nt, adj_off, adj, tris, ne, layers, centroids, counts,
+                            nullptr, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *adj_off,
+                             const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
+                             int32_t centroids, const int64_t *off, int64_t *idx,
+                             fm_stream_t stream) {
+    return fm::launch_patch(true, seed, nt, adj_off, adj, tris, ne, layers, centroids, nullptr,
+                            off, idx, (cudaStream_t)stream);
+}

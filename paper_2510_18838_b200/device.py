@@ -448,3 +448,49 @@ def fp64_probe(blocks=148 * 8, threads=256, iters=4096):
         best = ms if best is None else min(best, ms)
     flops = 2.0 * 8 * iters * blocks * threads
     return flops / (best * 1e-3) / 1e12
+
+
+@dataclass
+class PatchTopology:
+    """Device element adjacency for ElementPatch selection
+    (_PatchTopology.__init__, pointwise.py:193-200): each interior edge of
+    edge_tris links its two elements in both directions, as a CSR over
+    elements.  Neighbour order inside a row does not affect the patch."""
+
+    adj_off: torch.Tensor  # int64 (ne + 1)
+    adj: torch.Tensor  # int64
+    tris: torch.Tensor  # int64 (ne, 3)
+    ne: int
+
+    @classmethod
+    def from_mesh_arrays(cls, tris, edge_tris):
+        tris = to_device(tris, torch.int64).reshape(-1, 3)
+        et = to_device(edge_tris, torch.int64).reshape(-1, 2)
+        ne = int(tris.shape[0])
+        et = et[et[:, 1] >= 0]
+        src = torch.cat([et[:, 0], et[:, 1]])
+        dst = torch.cat([et[:, 1], et[:, 0]])
+        order = torch.argsort(src, stable=True)
+        counts = torch.bincount(src, minlength=ne)
+        adj_off = torch.zeros(ne + 1, dtype=torch.int64, device=tris.device)
+        torch.cumsum(counts, 0, out=adj_off[1:])
+        return cls(adj_off, dst[order].contiguous(), tris.contiguous(), ne)
+
+
+def patch_supports(topo, seed, layers, centroids):
+    """ElementPatch support CSR on the device (fm_patch_count / fm_patch_fill;
+    pointwise.py:212-230): (offsets int64 (nt+1), idx int64, counts int64 (nt),
+    -1 where a patch exceeds FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)."""
+    L = _lib.lib()
+    seed = to_device(seed, torch.int64)
+    nt = int(seed.shape[0])
+    counts = torch.empty(nt, dtype=torch.int64, device=seed.device)
+    args = (ptr(seed), nt, ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris), topo.ne,
+            int(layers), int(bool(centroids)))
+    check(L.fm_patch_count(*args, ptr(counts), _stream()), "fm_patch_count")
+    offsets = torch.zeros(nt + 1, dtype=torch.int64, device=seed.device)
+    torch.cumsum(counts.clamp_min(0), 0, out=offsets[1:])
+    nnz = int(offsets[-1]) if nt else 0
+    idx = torch.empty(nnz, dtype=torch.int64, device=seed.device)
+    check(L.fm_patch_fill(*args, ptr(offsets), ptr(idx), _stream()), "fm_patch_fill")
+    return offsets, idx, counts

@@ -142,3 +142,56 @@ class PointGrid:
 def build_point_grid(points, cells_per_point=1.0):
     """locate.py:171-172."""
     return PointGrid(points, cells_per_point)
+
+
+# locate.py:31: element bboxes are padded by this fraction of the diameter
+BBOX_PAD_REL = 1e-9
+
+
+class ElementGrid:
+    """The reference's element acceleration grid (`UniformGrid` /
+    `build_grid`, locate.py:111-141, 164-168, CSR layout 65-84), built with
+    tensor ops on the device: each element enters every cell its padded bbox
+    overlaps; cells row-major (iy*nx + ix), items ascending per cell.  Same
+    geometry and arithmetic as the reference, so `fm_locate_batch` on it
+    returns what the reference's `locate_arrays` returns."""
+
+    def __init__(self, mesh, cells_per_element=1.0, device=None):
+        import torch
+
+        if cells_per_element <= 0:
+            raise ValueError("cells_per_element must be > 0")
+        bbox = np.asarray(mesh.bbox, dtype=np.float64)
+        lo, hi = _pad_bbox(bbox[0], bbox[1])
+        nx, ny = _grid_shape_2d(lo, hi, int(mesh.tri_xy.shape[0]), cells_per_element)
+        self.lo, self.hi, self.nx, self.ny = lo, hi, nx, ny
+        self.dx = (hi[0] - lo[0]) / nx
+        self.dy = (hi[1] - lo[1]) / ny
+        self.mesh = mesh
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = torch.as_tensor(np.array(mesh.tri_xy, dtype=np.float64), device=dev)
+        pad = BBOX_PAD_REL * torch.as_tensor(
+            np.array(mesh.diameters, dtype=np.float64), device=dev)
+
+        def span(axis, d, n):
+            c = t[:, :, axis]
+            c0 = ((c.amin(dim=1) - pad - float(lo[axis])) / d).to(torch.int64).clamp(0, n - 1)
+            c1 = ((c.amax(dim=1) + pad - float(lo[axis])) / d).to(torch.int64).clamp(0, n - 1)
+            return c0, c1
+
+        ex0, ex1 = span(0, self.dx, nx)
+        ey0, ey1 = span(1, self.dy, ny)
+        wx = ex1 - ex0 + 1
+        counts = wx * (ey1 - ey0 + 1)
+        ne = t.shape[0]
+        items = torch.repeat_interleave(torch.arange(ne, device=dev), counts)
+        start = torch.cumsum(counts, 0) - counts
+        k = torch.arange(items.shape[0], device=dev) - start[items]
+        cells = (ey0[items] + k // wx[items]) * nx + ex0[items] + k % wx[items]
+        # (cell, id) order: entries are generated in ascending id, so a stable
+        # sort by cell is the reference's lexsort (locate.py:79)
+        order = torch.argsort(cells, stable=True)
+        self.cell_items = items[order].contiguous()
+        off = torch.zeros(nx * ny + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(torch.bincount(cells, minlength=nx * ny), 0, out=off[1:])
+        self.cell_offsets = off

@@ -235,7 +235,29 @@ def locate_cases():
     save("locate", **out)
 
 
+def patch_cases():
+    """ElementPatch supports: the reference's own _PatchTopology.patch_dofs
+    (pointwise.py:190-230) for every element of two meshes as seed, layers
+    1-3, vertex and centroid dofs."""
+    from fieldbridge.pointwise import _PatchTopology
+
+    out = {}
+    for name, m in (("sq", fb.square(12)), ("disk", fb.disk(1.0, 6))):
+        out[f"{name}_tris"] = m.tris
+        out[f"{name}_edge_tris"] = m.edge_tris
+        seeds = np.arange(m.tris.shape[0], dtype=np.int64)
+        for loc in ("vertices", "centroids"):
+            topo = _PatchTopology(m, loc)
+            for layers in (1, 2, 3):
+                parts = [topo.patch_dofs(int(s), layers) for s in seeds]
+                off = np.concatenate([[0], np.cumsum([p.size for p in parts])]).astype(np.int64)
+                out[f"{name}_{loc}_{layers}_off"] = off
+                out[f"{name}_{loc}_{layers}_idx"] = np.concatenate(parts).astype(np.int64)
+    save("patch", **out)
+
+
 if __name__ == "__main__":
+    patch_cases()
     locate_cases()
     rbf_table()
     disk_small()

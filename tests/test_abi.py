@@ -1,8 +1,9 @@
-"""CPU: the C-ABI library loads and exports every function include/fieldmap.h
+"""CPU: the C-ABI library loads and exports every function include/*.h
 declares (no compute calls: there is no GPU here), and the ctypes structs
 match the header's layout."""
 
 import ctypes
+import glob
 import os
 import re
 
@@ -10,11 +11,11 @@ import pytest
 
 from conftest import ROOT
 
-HEADER = os.path.join(ROOT, "include", "fieldmap.h")
+HEADERS = sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def _declared_functions():
-    text = open(HEADER).read()
+    text = "".join(open(h).read() for h in HEADERS)
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(fm_[a-z0-9_]+)\s*\(", text)))
 

@@ -656,3 +656,74 @@ def test_prepared_transfer_all_size_buckets_and_overflow():
     for lo, hi in zip([0] + edges, edges + [10 ** 9]):
         b = ok & (counts > lo) & (counts <= hi)
         assert not b.any() or err[b].max() < VALUE_RTOL, (lo, hi, err[b].max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["sq", "disk"])
+@pytest.mark.parametrize("loc", ["vertices", "centroids"])
+@pytest.mark.parametrize("layers", [1, 2, 3])
+def test_patch_supports_bitwise(name, loc, layers):
+    """fm_patch_count/fill vs the reference's own _PatchTopology.patch_dofs
+    (pointwise.py:190-230, golden fixture), every element as seed: the
+    support CSR (offsets, ids) bitwise."""
+    d = golden("patch")
+    tris = d[f"{name}_tris"]
+    seeds = np.arange(tris.shape[0])
+    off, idx, _ = Kb.patch_supports(seeds, tris, d[f"{name}_edge_tris"], layers,
+                                    loc == "centroids")
+    assert off.dtype == np.int64 and idx.dtype == np.int64
+    assert np.array_equal(off, d[f"{name}_{loc}_{layers}_off"])
+    assert np.array_equal(idx, d[f"{name}_{loc}_{layers}_idx"])
+
+
+@pytest.mark.gpu
+def test_patch_supports_random_seeds_and_overflow():
+    """20k random seeds (repeats, any order) at layers 1-4: GPU == oracle; a
+    patch beyond the per-target bound raises instead of truncating."""
+    from paper_2510_18838_b200._lib import FieldmapError
+
+    d = golden("patch")
+    tris, et = d["disk_tris"], d["disk_edge_tris"]
+    seeds = np.random.default_rng(5).integers(0, tris.shape[0], 20000)
+    for layers in (1, 4):
+        for cen in (False, True):
+            off, idx, _ = Kb.patch_supports(seeds, tris, et, layers, cen)
+            w_off, w_idx = O.patch_supports(seeds, et, tris, layers, cen)
+            assert np.array_equal(off, w_off) and np.array_equal(idx, w_idx)
+    off, idx, _ = Kb.patch_supports(np.array([], np.int64), tris, et, 1, False)
+    assert off.tolist() == [0] and idx.size == 0
+    with pytest.raises(FieldmapError):
+        Kb.patch_supports(seeds[:10], tris, et, 12, True)
+
+
+@pytest.mark.gpu
+def test_element_patch_locate_fit_chain():
+    """The reference's ElementPatch flow (_select_batch 271-296 then
+    _fit_batch 299-314) on device: locate_batch -> patch supports (unit
+    weights) -> fit_many, vs the same chain on the CPU oracle."""
+    d = golden("locate")
+    p = golden("patch")
+    rng = np.random.default_rng(11)
+    t = rng.uniform(0.02, 0.98, (3000, 2))
+    g, gn = d["sq_grid"], d["sq_grid_n"]
+    args = (d["sq_tri_xy"], d["sq_tris"], d["sq_tri_edges"], d["sq_vert_gid"], d["sq_tri_gid"],
+            d["sq_inv2a"], d["sq_epsfac"], float(g[0]), float(g[1]), float(g[2]), float(g[3]),
+            int(gn[0]), int(gn[1]), d["sq_cell_off"], d["sq_cell_items"], 1e-10)
+    found, elem, _, _, _ = Kb.locate_batch(t, *args)
+    assert found.all()
+    # vertex coordinates in vertex-id order, recovered from tri_xy / tris
+    tris = p["sq_tris"]
+    nv = int(tris.max()) + 1
+    xy = np.empty((nv, 2))
+    xy[tris.reshape(-1)] = d["sq_tri_xy"].reshape(-1, 2)
+    f = np.sin(xy[:, 0]) * np.cos(xy[:, 1]) + 2
+    off, idx, _ = Kb.patch_supports(elem, tris, p["sq_edge_tris"], 2, False)
+    w = np.ones(idx.size)
+    v, c, s = Kb.fit_many(t, off, idx, w, xy, f, 2, 0.0, True)
+    w_off, w_idx = O.patch_supports(elem, p["sq_edge_tris"], tris, 2, False)
+    assert np.array_equal(off, w_off) and np.array_equal(idx, w_idx)
+    wv, wc, ws = O.fit_many(t, w_off, w_idx, w, xy, f, 2, 0.0, True)
+    assert np.array_equal(s, ws)
+    ok = s == 0
+    assert ok.mean() > 0.99
+    np.testing.assert_allclose(v[ok], wv[ok], rtol=1e-10, atol=0)

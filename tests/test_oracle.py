@@ -194,3 +194,17 @@ def test_oracle_locate_batch_bitwise(name, tol):
         want = d[f"{name}_{tol:g}_{k}"]
         assert a.dtype == want.dtype
         assert np.array_equal(a, want, equal_nan=(k == "bary")), k
+
+
+@pytest.mark.parametrize("name", ["sq", "disk"])
+@pytest.mark.parametrize("loc", ["vertices", "centroids"])
+@pytest.mark.parametrize("layers", [1, 2, 3])
+def test_oracle_patch_supports_bitwise(name, loc, layers):
+    """ElementPatch restatement vs the reference's own _PatchTopology.patch_dofs
+    (pointwise.py:190-230) for every element as seed."""
+    d = golden("patch")
+    tris = d[f"{name}_tris"]
+    seeds = np.arange(tris.shape[0])
+    off, idx = O.patch_supports(seeds, d[f"{name}_edge_tris"], tris, layers, loc == "centroids")
+    assert np.array_equal(off, d[f"{name}_{loc}_{layers}_off"])
+    assert np.array_equal(idx, d[f"{name}_{loc}_{layers}_idx"])
