@@ -464,8 +464,10 @@ class PatchTopology:
 
     @classmethod
     def from_mesh_arrays(cls, tris, edge_tris):
-        tris = to_device(tris, torch.int64).reshape(-1, 3)
-        et = to_device(edge_tris, torch.int64).reshape(-1, 2)
+        i64 = lambda a: to_device(  # noqa: E731
+            a if isinstance(a, torch.Tensor) else np.array(a, dtype=np.int64), torch.int64)
+        tris = i64(tris).reshape(-1, 3)
+        et = i64(edge_tris).reshape(-1, 2)
         ne = int(tris.shape[0])
         et = et[et[:, 1] >= 0]
         src = torch.cat([et[:, 0], et[:, 1]])
@@ -494,3 +496,28 @@ def patch_supports(topo, seed, layers, centroids):
     idx = torch.empty(nnz, dtype=torch.int64, device=seed.device)
     check(L.fm_patch_fill(*args, ptr(offsets), ptr(idx), _stream()), "fm_patch_fill")
     return offsets, idx, counts
+
+
+def locate_elements(eg, mesh, pts, tol=1e-10):
+    """fm_locate_batch on device points over an element grid (the caller's
+    locate_arrays, locate.py:175-186, DEFAULT_TOL 1e-10 at locate.py:28):
+    (found u8, elem int64) device tensors."""
+    L = _lib.lib()
+    n = int(pts.shape[0])
+    dev = pts.device
+    f64 = lambda a: to_device(a, torch.float64)  # noqa: E731
+    i64 = lambda a: to_device(  # noqa: E731
+        a if isinstance(a, torch.Tensor) else np.array(a, dtype=np.int64), torch.int64)
+    arrs = [f64(mesh.tri_xy), i64(mesh.tris), i64(mesh.tri_edges), i64(mesh.vert_gid),
+            i64(mesh.tri_gid), f64(mesh.inv2a), f64(mesh.epsfac)]
+    cell_off, cell_items = i64(eg.cell_offsets), i64(eg.cell_items)
+    found = _empty(n, torch.uint8, dev)
+    elem = _empty(n, torch.int64, dev)
+    dim = _empty(n, torch.int64, dev)
+    ent = _empty(n, torch.int64, dev)
+    bary = _empty((n, 3), torch.float64, dev)
+    check(L.fm_locate_batch(ptr(pts), n, *[ptr(a) for a in arrs], float(eg.lo[0]),
+                            float(eg.lo[1]), float(eg.dx), float(eg.dy), int(eg.nx), int(eg.ny),
+                            ptr(cell_off), ptr(cell_items), float(tol), ptr(found), ptr(elem),
+                            ptr(dim), ptr(ent), ptr(bary), _stream()), "fm_locate_batch")
+    return found.bool(), elem

@@ -15,9 +15,10 @@ fields with several components ((n, C) values -> (nt, C) results).
 Differences that are not extensions:
   * `threads` is accepted and ignored (the GPU path has no host chunking;
     results are the reference's threads=1 results).
-  * ElementPatch selection on mesh-backed sources is SURVEY.md §8(f) "next";
-    it raises NotImplementedError (point clouds raise FieldError exactly like
-    the reference).
+  * ElementPatch selection runs on the device:
+    element grid, fm_locate_batch, fm_patch_count/fill, fm_fit_many; a patch
+    beyond FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS raises FieldmapError, and
+    transfer_extrinsic with ElementPatch raises NotImplementedError.
 """
 
 import enum
@@ -237,14 +238,88 @@ def _r_max_device(cloud, targets, tbbox=None):
 
 
 def _check_patch(fitspec, mesh):
+    """True when the selection is ElementPatch on mesh-backed sources (the
+    patch path); FieldError for ElementPatch on a bare point cloud
+    (pointwise.py:272-275)."""
     if isinstance(fitspec.selection, ElementPatch):
         if mesh is None:
             raise FieldError(
                 "element-patch selection needs mesh-backed source dofs, not "
                 "a bare point cloud")
-        raise NotImplementedError(
-            "ElementPatch selection on mesh-backed sources is not on the B200 path yet "
-            "(SURVEY.md §8(f) rank 2)")
+        return True
+    return False
+
+
+class _PatchSupports:
+    """_select_batch's ElementPatch branch (pointwise.py:271-296) on the
+    device: the element grid (the caller's reference UniformGrid for this
+    mesh, else the same grid built on the device, locate.py:111-141,
+    164-168), fm_locate_batch for each target's element, fm_patch_count/fill
+    for the patch dofs (pointwise.py:212-230), unit weights.  Errors are the
+    reference's, naming the first failing target."""
+
+    def __init__(self, targets, fitspec, mesh, source_location, grid=None, base_index=0):
+        from .locate import ElementGrid
+
+        if targets.shape[1] != 2:
+            raise FieldError("element-patch selection is 2-D (triangle meshes)")
+        if grid is not None and getattr(grid, "mesh", None) is mesh and hasattr(
+                grid, "cell_items") and not isinstance(grid, PointGrid):
+            eg = grid
+        else:
+            eg = ElementGrid(mesh)
+        t = D.to_device(targets)
+        found, elem = D.locate_elements(eg, mesh, t)
+        found_h = found.cpu().numpy()
+        if not found_h.all():
+            i = int(np.argmax(~found_h))
+            raise InsufficientSourcesError(
+                f"{_point_label(targets, i)} (index {base_index + i}) lies "
+                "outside the source mesh; element-patch selection needs a "
+                "containing element")
+        topo = D.PatchTopology.from_mesh_arrays(mesh.tris, mesh.edge_tris)
+        self.offsets, self.idx, counts = D.patch_supports(
+            topo, elem, fitspec.selection.layers, source_location == "centroids")
+        counts_h = counts.cpu().numpy()
+        if (counts_h < 0).any():
+            from ._lib import FieldmapError
+
+            i = int(np.argmax(counts_h < 0))
+            raise FieldmapError(
+                f"{_point_label(targets, i)} (index {base_index + i}): element patch exceeds "
+                "the kernel's per-target bound (FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)")
+        need = n_monomials(fitspec.degree)
+        if (counts_h < need).any():
+            i = int(np.argmax(counts_h < need))
+            raise UnderdeterminedError(
+                f"{_point_label(targets, i)} (index {base_index + i}) patch "
+                f"has {counts_h[i]} dofs; a degree-{fitspec.degree} fit needs "
+                f"at least {need}")
+        self.targets = targets
+        self.t = t
+        self.fitspec = fitspec
+        self.base_index = base_index
+        self.max_m = int(counts_h.max()) if counts_h.size else 0
+        self.w = torch.ones(self.idx.shape[0], dtype=torch.float64, device=t.device)
+
+    def host(self):
+        return (self.offsets.cpu().numpy(), self.idx.cpu().numpy(), self.w.cpu().numpy())
+
+    def values(self, src_xy, src_vals):
+        """_fit_batch (pointwise.py:299-314) per component on the patch CSR."""
+        src = D.to_device(src_xy)
+        vals = D.to_device(src_vals)
+        cols = vals.reshape(vals.shape[0], -1)
+        out = []
+        for c in range(cols.shape[1]):
+            v, _, status, _ = D.fit_many(self.t, self.offsets, self.idx, self.w, src,
+                                         cols[:, c].contiguous(), self.fitspec.degree,
+                                         float(self.fitspec.lam), bool(self.fitspec.centering),
+                                         self.max_m)
+            _raise_status(status.cpu().numpy(), self.targets, self.fitspec, self.base_index)
+            out.append(v)
+        y = torch.stack(out, dim=1) if vals.ndim > 1 else out[0]
+        return y.reshape((self.t.shape[0],) + tuple(vals.shape[1:]))
 
 
 class _Plan:
@@ -354,9 +429,10 @@ def select_support(target, source_points, selection, rbf=None, grid=None, fit_de
     t = np.asarray(tuple(target), dtype=np.float64)[None, :]
     rbf = rbf if rbf is not None else RadialBasisSpec(RbfKind.CONST, r_c=None)
     spec = FitSpec(fit_degree, rbf, selection)
-    _check_patch(spec, mesh)
-    plan = _Plan(src, t, spec, grid)
-    off, idx, w = plan.supports()
+    if _check_patch(spec, mesh):
+        off, idx, w = _PatchSupports(t, spec, mesh, source_location, grid).host()
+    else:
+        off, idx, w = _Plan(src, t, spec, grid).supports()
     return idx[off[0]:off[1]], w[off[0]:off[1]]
 
 
@@ -412,16 +488,22 @@ class PreparedTransfer:
             self.src_xy = _as_points(source_points)
             self.targets = _as_points(target_points, self.src_xy.shape[1])
         self.fitspec = fitspec
-        _check_patch(fitspec, mesh)
+        self._support = None
+        self._patch = None
+        if _check_patch(fitspec, mesh):
+            # ElementPatch: the patch CSR stays on the device; apply re-solves
+            # per component like the reference (pointwise.py:416, 422-431)
+            self._patch = _PatchSupports(self.targets, fitspec, mesh, source_location, grid)
+            return
         self._plan = _Plan(self.src_xy, self.targets, fitspec, grid)
         self.operator, self._stats = self._plan.build_operator()
-        self._support = None
 
     @property
     def support(self):
         """(offsets, idx, raw weights), as the reference's PreparedTransfer.support."""
         if self._support is None:
-            self._support = self._plan.supports()
+            self._support = (self._patch.host() if self._patch is not None else
+                             self._plan.supports())
         return self._support
 
     def _check_fit(self):
@@ -432,6 +514,13 @@ class PreparedTransfer:
         """Transfer values (ns,) or (ns, C).  numpy in -> numpy out; CUDA
         tensor in -> CUDA tensor out (no host round trip); host tensor in
         (pinned: async copies) -> pinned host tensor out."""
+        if self._patch is not None:
+            if source_values.shape[0] != self.src_xy.shape[0]:
+                raise FieldError("source values disagree with prepared points")
+            y = self._patch.values(self.src_xy, source_values)
+            if isinstance(source_values, torch.Tensor):
+                return y if source_values.is_cuda else y.cpu()
+            return y.cpu().numpy()
         if isinstance(source_values, torch.Tensor):
             if source_values.shape[0] != self.src_xy.shape[0]:
                 raise FieldError("source values disagree with prepared points")
@@ -470,7 +559,7 @@ def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=N
     operator build."""
     if any(isinstance(a, torch.Tensor) for a in (source_points, source_values, target_points)):
         return _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec,
-                                        grid, mesh)
+                                        grid, mesh, source_location)
     src_xy = _as_points(source_points)
     src_vals = np.ascontiguousarray(source_values, dtype=np.float64)
     if src_xy.shape[0] == 0:
@@ -478,9 +567,12 @@ def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=N
     if src_xy.shape[0] != src_vals.shape[0]:
         raise FieldError("source points and values disagree in length")
     targets = _as_points(target_points, src_xy.shape[1])
-    _check_patch(fitspec, mesh)
+    patch = _check_patch(fitspec, mesh)
     if targets.shape[0] == 0:
         return np.empty((0,) + src_vals.shape[1:], dtype=np.float64)
+    if patch:
+        ps = _PatchSupports(targets, fitspec, mesh, source_location, grid)
+        return ps.values(src_xy, src_vals).cpu().numpy()
     plan = _Plan(src_xy, targets, fitspec, grid)
     if src_vals.ndim == 1:
         values, status, stats = plan.transfer_scalar(D.to_device(src_vals))
@@ -493,7 +585,8 @@ def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=N
     return op.apply(D.to_device(src_vals)).cpu().numpy()
 
 
-def _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec, grid, mesh):
+def _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec, grid, mesh,
+                             source_location="vertices"):
     as_t = lambda a: a if isinstance(a, torch.Tensor) else torch.from_numpy(  # noqa: E731
         np.ascontiguousarray(a, dtype=np.float64))
     sp, sv, tp = as_t(source_points), as_t(source_values), as_t(target_points)
@@ -502,7 +595,10 @@ def _fit_point_cloud_tensors(source_points, source_values, target_points, fitspe
         raise InsufficientSourcesError("no source points")
     if sp.shape[0] != sv.shape[0]:
         raise FieldError("source points and values disagree in length")
-    _check_patch(fitspec, mesh)
+    if _check_patch(fitspec, mesh):
+        ps = _PatchSupports(tp.reshape(-1, 2), fitspec, mesh, source_location, grid)
+        y = ps.values(sp, sv)
+        return y.cpu() if host_out else y
     main = torch.cuda.current_stream()
     # the geometry goes first (the pipeline starts on it); the field's copy
     # follows on a side stream and overlaps the selection and build
@@ -560,7 +656,9 @@ def transfer_extrinsic(evaluate_callback, target_points, fitspec, source_points,
         raise InsufficientSourcesError("no source points")
     targets = _as_points(target_points, src_xy.shape[1])
     nt = targets.shape[0]
-    _check_patch(fitspec, mesh)
+    if _check_patch(fitspec, mesh):
+        raise NotImplementedError("transfer_extrinsic with ElementPatch selection is not on "
+                                  "the B200 path (SURVEY.md §8(f) rank 3)")
     cloud = D.SourceCloud(src_xy)
     grid = _GridHandle(cloud)
     out = np.empty(nt, dtype=np.float64)

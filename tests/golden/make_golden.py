@@ -253,6 +253,42 @@ def patch_cases():
                 off = np.concatenate([[0], np.cumsum([p.size for p in parts])]).astype(np.int64)
                 out[f"{name}_{loc}_{layers}_off"] = off
                 out[f"{name}_{loc}_{layers}_idx"] = np.concatenate(parts).astype(np.int64)
+    # the public API on ElementPatch (pointwise.py:434-451, 317-336):
+    # fit_point_cloud values and select_support, with the mesh arrays the
+    # device path needs (tests rebuild a mesh-like namespace from them)
+    from fieldbridge.pointwise import (ElementPatch, FitSpec, RadialBasisSpec, RbfKind,
+                                       fit_point_cloud, select_support)
+
+    for name, m in (("sq", fb.square(12)), ("disk", fb.disk(1.0, 6))):
+        for k in ("coords", "tri_xy", "tri_edges", "vert_gid", "tri_gid", "inv2a", "epsfac",
+                  "diameters", "bbox"):
+            out[f"{name}_{k}"] = getattr(m, k)
+        g = fb.build_grid(m)
+        out[f"{name}_grid"] = np.array([g.lo[0], g.lo[1], g.dx, g.dy])
+        out[f"{name}_grid_n"] = np.array([g.nx, g.ny])
+        out[f"{name}_cell_off"] = g.cell_offsets
+        out[f"{name}_cell_items"] = g.cell_items
+        rng = np.random.RandomState(13)
+        if name == "sq":
+            t = rng.uniform(0.0, 1.0, (500, 2))
+        else:
+            r = 0.95 * np.sqrt(rng.uniform(0, 1, 500))
+            a = rng.uniform(0, 2 * np.pi, 500)
+            t = np.stack([r * np.cos(a), r * np.sin(a)], axis=1)
+        out[f"{name}_targets"] = t
+        cen = m.centroids()
+        out[f"{name}_centroids"] = cen
+        for loc, src in (("vertices", m.coords), ("centroids", cen)):
+            f = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+            for deg, layers in ((1, 2), (2, 3)):
+                spec = FitSpec(deg, RadialBasisSpec(RbfKind.CONST, r_c=None),
+                               ElementPatch(layers))
+                out[f"{name}_{loc}_fit_{deg}_{layers}"] = fit_point_cloud(
+                    src, f, t, spec, mesh=m, source_location=loc)
+            idx, w = select_support(t[0], src, ElementPatch(2), fit_degree=2, mesh=m,
+                                    source_location=loc)
+            out[f"{name}_{loc}_sel_idx"] = idx
+            out[f"{name}_{loc}_sel_w"] = w
     save("patch", **out)
 
 

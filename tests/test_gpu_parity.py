@@ -727,3 +727,73 @@ def test_element_patch_locate_fit_chain():
     ok = s == 0
     assert ok.mean() > 0.99
     np.testing.assert_allclose(v[ok], wv[ok], rtol=1e-10, atol=0)
+
+
+def _golden_mesh(d, name):
+    from types import SimpleNamespace
+
+    keys = ("tris", "edge_tris", "tri_xy", "tri_edges", "vert_gid", "tri_gid", "inv2a", "epsfac",
+            "diameters", "bbox")
+    return SimpleNamespace(**{k: d[f"{name}_{k}"] for k in keys})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["sq", "disk"])
+@pytest.mark.parametrize("loc", ["vertices", "centroids"])
+def test_fit_point_cloud_element_patch_vs_reference(name, loc):
+    """fit_point_cloud with ElementPatch on a mesh (pointwise.py:271-296 +
+    434-451) vs the reference's own outputs: values within 1e-10 rel;
+    select_support bitwise; PreparedTransfer.apply (2 components, numpy and
+    CUDA tensors) equal to the per-component values."""
+    import torch
+
+    d = golden("patch")
+    mesh = _golden_mesh(d, name)
+    src = d[f"{name}_coords"] if loc == "vertices" else d[f"{name}_centroids"]
+    t = d[f"{name}_targets"]
+    f = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    for deg, layers in ((1, 2), (2, 3)):
+        spec = P.FitSpec(deg, P.RadialBasisSpec(P.RbfKind.CONST, r_c=None),
+                         P.ElementPatch(layers))
+        got = P.fit_point_cloud(src, f, t, spec, mesh=mesh, source_location=loc)
+        want = d[f"{name}_{loc}_fit_{deg}_{layers}"]
+        np.testing.assert_allclose(got, want, rtol=1e-10, atol=0)
+        pt = P.PreparedTransfer(src, t, spec, mesh=mesh, source_location=loc)
+        two = np.stack([f, 2 * f + 1], axis=1)
+        y = pt.apply(two)
+        np.testing.assert_allclose(y[:, 0], want, rtol=1e-10, atol=0)
+        np.testing.assert_allclose(y[:, 1], 2 * got + 1, rtol=1e-12, atol=1e-12)
+        yt = P.fit_point_cloud(torch.from_numpy(src).cuda(), torch.from_numpy(f).cuda(),
+                               torch.from_numpy(t).cuda(), spec, mesh=mesh, source_location=loc)
+        assert yt.is_cuda and np.array_equal(yt.cpu().numpy(), got)
+    idx, w = P.select_support(t[0], src, P.ElementPatch(2), fit_degree=2, mesh=mesh,
+                              source_location=loc)
+    assert np.array_equal(idx, d[f"{name}_{loc}_sel_idx"])
+    assert np.array_equal(w, d[f"{name}_{loc}_sel_w"])
+
+
+@pytest.mark.gpu
+def test_element_patch_errors_match_reference():
+    """The reference's ElementPatch errors: too few patch dofs ->
+    UnderdeterminedError naming the first target (message measured on the
+    reference: 'target 86 at (0.00984544, 0.994239) (index 86) patch has 2
+    dofs; a degree-1 fit needs at least 3'); a target outside the mesh ->
+    InsufficientSourcesError; no mesh -> FieldError."""
+    from paper_2510_18838_b200.errors import (FieldError, InsufficientSourcesError,
+                                              UnderdeterminedError)
+
+    d = golden("patch")
+    mesh = _golden_mesh(d, "sq")
+    src, t = d["sq_centroids"], d["sq_targets"]
+    f = np.ones(src.shape[0])
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.CONST, r_c=None), P.ElementPatch(1))
+    with pytest.raises(UnderdeterminedError) as e:
+        P.fit_point_cloud(src, f, t, spec, mesh=mesh, source_location="centroids")
+    assert str(e.value) == ("target 86 at (0.00984544, 0.994239) (index 86) patch has 2 dofs; "
+                            "a degree-1 fit needs at least 3")
+    spec2 = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.CONST, r_c=None), P.ElementPatch(2))
+    with pytest.raises(InsufficientSourcesError):
+        P.fit_point_cloud(src, f, np.array([[0.5, 0.5], [1.5, 0.5]]), spec2, mesh=mesh,
+                          source_location="centroids")
+    with pytest.raises(FieldError):
+        P.fit_point_cloud(src, f, t, spec2)

@@ -208,3 +208,28 @@ def test_oracle_patch_supports_bitwise(name, loc, layers):
     off, idx = O.patch_supports(seeds, d[f"{name}_edge_tris"], tris, layers, loc == "centroids")
     assert np.array_equal(off, d[f"{name}_{loc}_{layers}_off"])
     assert np.array_equal(idx, d[f"{name}_{loc}_{layers}_idx"])
+
+
+def _golden_mesh(d, name):
+    from types import SimpleNamespace
+
+    keys = ("tris", "edge_tris", "tri_xy", "tri_edges", "vert_gid", "tri_gid", "inv2a", "epsfac",
+            "diameters", "bbox")
+    return SimpleNamespace(**{k: d[f"{name}_{k}"] for k in keys})
+
+
+@pytest.mark.parametrize("name", ["sq", "disk"])
+def test_element_grid_matches_reference_uniform_grid(name):
+    """ElementGrid (tensor ops; run here on CPU tensors) == the reference's
+    UniformGrid (locate.py:111-141): geometry and cell CSR bitwise."""
+    import torch
+
+    from paper_2510_18838_b200.locate import ElementGrid
+
+    d = golden("patch")
+    eg = ElementGrid(_golden_mesh(d, name), device=torch.device("cpu"))
+    g, gn = d[f"{name}_grid"], d[f"{name}_grid_n"]
+    assert (eg.nx, eg.ny) == (int(gn[0]), int(gn[1]))
+    assert [eg.lo[0], eg.lo[1], eg.dx, eg.dy] == g.tolist()
+    assert np.array_equal(eg.cell_offsets.numpy(), d[f"{name}_cell_off"])
+    assert np.array_equal(eg.cell_items.numpy(), d[f"{name}_cell_items"])
