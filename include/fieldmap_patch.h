@@ -23,20 +23,24 @@ extern "C" {
 
 /* Per target i with containing element seed[i] (locate_batch's `elem`,
  * int64, >= 0): the elements within `layers` hops over the element
- * adjacency CSR (adj_off int64 (ne+1), adj int64 -- each interior edge
+ * adjacency CSR (adj_off int32 (ne+1), adj int32 -- each interior edge
  * contributes both directions, pointwise.py:195-200), sorted ascending
  * (pointwise.py:226); dofs = those element ids when `centroids` != 0, else
- * the sorted distinct vertex ids of tris[elems] (tris int64 (ne, 3),
- * pointwise.py:229).
+ * the sorted distinct vertex ids of tris[elems] (tris int32 (ne, 3),
+ * pointwise.py:229).  The topology is int32 (the Python shim converts the
+ * reference's int64 arrays once) so it stays L2-resident.  `order` (int64
+ * permutation of 0..nt-1, or NULL) is the processing order -- e.g. targets
+ * sorted by seed element, for L2 locality; outputs stay at each target's own
+ * position, so results never depend on it.
  *   fm_patch_count: counts int64 (nt) (-1 on overflow).
  *   fm_patch_fill:  idx int64 at off[i] .. off[i+1] (off = exclusive scan of
  *                   counts, int64 (nt+1)).  Bitwise equal to the reference. */
-int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *adj_off, const int64_t *adj,
-                   const int64_t *tris, int64_t ne, int32_t layers, int32_t centroids,
-                   int64_t *counts, fm_stream_t stream);
-int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *adj_off, const int64_t *adj,
-                  const int64_t *tris, int64_t ne, int32_t layers, int32_t centroids,
-                  const int64_t *off, int64_t *idx, fm_stream_t stream);
+int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *order, const int32_t *adj_off,
+                   const int32_t *adj, const int32_t *tris, int64_t ne, int32_t layers,
+                   int32_t centroids, int64_t *counts, fm_stream_t stream);
+int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *order, const int32_t *adj_off,
+                  const int32_t *adj, const int32_t *tris, int64_t ne, int32_t layers,
+                  int32_t centroids, const int64_t *off, int64_t *idx, fm_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -90,9 +90,10 @@ SIGNATURES = {
     "fm_apply": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
     "fm_fp64_probe": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp]),
     # include/fieldmap_patch.h
-    "fm_patch_count": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]),
-    "fm_patch_fill": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp,
-                              c_vp]),
+    "fm_patch_count": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp,
+                               c_vp]),
+    "fm_patch_fill": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp,
+                              c_vp, c_vp]),
     "fm_locate_batch": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64,
                                 c_f64, c_f64, c_f64, c_i64, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp,
                                 c_vp, c_vp, c_vp, c_vp]),

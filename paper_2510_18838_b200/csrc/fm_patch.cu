@@ -22,24 +22,26 @@ namespace fm {
 
 template <bool FILL>
 __global__ void __launch_bounds__(128)
-    k_patch(const int64_t *__restrict__ seed, int64_t nt, const int64_t *__restrict__ adj_off,
-            const int64_t *__restrict__ adj, const int64_t *__restrict__ tris, int32_t layers,
+    k_patch(const int64_t *__restrict__ seed, int64_t nt, const int64_t *__restrict__ order,
+            const int32_t *__restrict__ adj_off, const int32_t *__restrict__ adj,
+            const int32_t *__restrict__ tris, int32_t layers,
             int32_t centroids, int64_t *__restrict__ counts, const int64_t *__restrict__ off,
             int64_t *__restrict__ idx) {
     int32_t el[FM_PATCH_MAX_ELEMS];
     int32_t dof[FM_PATCH_MAX_DOFS];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nt;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = order ? __ldg(order + p) : p;
         int n = 1;
         bool overflow = false;
-        el[0] = (int32_t)seed[i];
+        el[0] = (int32_t)__ldg(seed + i);
         int fs = 0, fe = 1;  // frontier [fs, fe)
         for (int layer = 0; layer < layers && !overflow && fs < fe; layer++) {
             for (int f = fs; f < fe && !overflow; f++) {
                 const int32_t t = el[f];
-                const int64_t a1 = __ldg(adj_off + t + 1);
-                for (int64_t a = __ldg(adj_off + t); a < a1; a++) {
-                    const int32_t nb = (int32_t)__ldg(adj + a);
+                const int32_t a1 = __ldg(adj_off + t + 1);
+                for (int32_t a = __ldg(adj_off + t); a < a1; a++) {
+                    const int32_t nb = __ldg(adj + a);
                     bool seen = false;
                     for (int q = 0; q < n; q++) seen |= (el[q] == nb);
                     if (seen) continue;
@@ -79,9 +81,9 @@ __global__ void __launch_bounds__(128)
         // np.unique(tris[elems]) (pointwise.py:229): sorted insert with dedup
         int m = 0;
         for (int a = 0; a < n && !overflow; a++) {
-            const int64_t *tv = tris + 3 * (int64_t)el[a];
+            const int32_t *tv = tris + 3 * (int64_t)el[a];
             for (int c = 0; c < 3; c++) {
-                const int32_t v = (int32_t)__ldg(tv + c);
+                const int32_t v = __ldg(tv + c);
                 int b = m - 1;
                 while (b >= 0 && dof[b] > v) b--;
                 if (b >= 0 && dof[b] == v) continue;
@@ -105,8 +107,9 @@ __global__ void __launch_bounds__(128)
     }
 }
 
-static int launch_patch(bool fill, const int64_t *seed, int64_t nt, const int64_t *adj_off,
-                        const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
+static int launch_patch(bool fill, const int64_t *seed, int64_t nt, const int64_t *order,
+                        const int32_t *adj_off, const int32_t *adj, const int32_t *tris,
+                        int64_t ne, int32_t layers,
                         int32_t centroids, int64_t *counts, const int64_t *off, int64_t *idx,
                         cudaStream_t stream) {
     if (nt < 0 || ne < 1 || layers < 1 || ne > INT32_MAX) return FM_ERR_ARG;
@@ -116,28 +119,30 @@ static int launch_patch(bool fill, const int64_t *seed, int64_t nt, const int64_
     const int threads = 128;
     const int blocks = (int)std::min<int64_t>((nt + threads - 1) / threads, (int64_t)kSMs * 16);
     if (fill)
-        k_patch<true><<<blocks, threads, 0, stream>>>(seed, nt, adj_off, adj, tris, layers,
-                                                      centroids, nullptr, off, idx);
+        k_patch<true><<<blocks, threads, 0, stream>>>(seed, nt, order, adj_off, adj, tris,
+                                                      layers, centroids, nullptr, off, idx);
     else
-        k_patch<false><<<blocks, threads, 0, stream>>>(seed, nt, adj_off, adj, tris, layers,
-                                                       centroids, counts, nullptr, nullptr);
+        k_patch<false><<<blocks, threads, 0, stream>>>(seed, nt, order, adj_off, adj, tris,
+                                                       layers, centroids, counts, nullptr,
+                                                       nullptr);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
 
 }  // namespace fm
 
-extern "C" int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *adj_off,
-                              const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
-                              int32_t centroids, int64_t *counts, fm_stream_t stream) {
-    return fm::launch_patch(false, seed, nt, adj_off, adj, tris, ne, layers, centroids, counts,
+extern "C" int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *order,
+                              const int32_t *adj_off, const int32_t *adj, const int32_t *tris,
+                              int64_t ne, int32_t layers, int32_t centroids, int64_t *counts,
+                              fm_stream_t stream) {
+    return fm::launch_patch(false, seed, nt, order, adj_off, adj, tris, ne, layers, centroids, counts,
                             nullptr, nullptr, (cudaStream_t)stream);
 }
 
-extern "C" int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *adj_off,
-                             const int64_t *adj, const int64_t *tris, int64_t ne, int32_t layers,
-                             int32_t centroids, const int64_t *off, int64_t *idx,
-                             fm_stream_t stream) {
-    return fm::launch_patch(true, seed, nt, adj_off, adj, tris, ne, layers, centroids, nullptr,
+extern "C" int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *order,
+                             const int32_t *adj_off, const int32_t *adj, const int32_t *tris,
+                             int64_t ne, int32_t layers, int32_t centroids, const int64_t *off,
+                             int64_t *idx, fm_stream_t stream) {
+    return fm::launch_patch(true, seed, nt, order, adj_off, adj, tris, ne, layers, centroids, nullptr,
                             off, idx, (cudaStream_t)stream);
 }

@@ -457,9 +457,9 @@ class PatchTopology:
     edge_tris links its two elements in both directions, as a CSR over
     elements.  Neighbour order inside a row does not affect the patch."""
 
-    adj_off: torch.Tensor  # int64 (ne + 1)
-    adj: torch.Tensor  # int64
-    tris: torch.Tensor  # int64 (ne, 3)
+    adj_off: torch.Tensor  # int32 (ne + 1)
+    adj: torch.Tensor  # int32
+    tris: torch.Tensor  # int32 (ne, 3)
     ne: int
 
     @classmethod
@@ -476,18 +476,24 @@ class PatchTopology:
         counts = torch.bincount(src, minlength=ne)
         adj_off = torch.zeros(ne + 1, dtype=torch.int64, device=tris.device)
         torch.cumsum(counts, 0, out=adj_off[1:])
-        return cls(adj_off, dst[order].contiguous(), tris.contiguous(), ne)
+        # int32 on the device: half the footprint, so the topology stays in L2
+        return cls(adj_off.to(torch.int32), dst[order].to(torch.int32).contiguous(),
+                   tris.to(torch.int32).contiguous(), ne)
 
 
-def patch_supports(topo, seed, layers, centroids):
+def patch_supports(topo, seed, layers, centroids, sort_by_seed=True):
     """ElementPatch support CSR on the device (fm_patch_count / fm_patch_fill;
     pointwise.py:212-230): (offsets int64 (nt+1), idx int64, counts int64 (nt),
-    -1 where a patch exceeds FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)."""
+    -1 where a patch exceeds FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS).
+    Targets are processed in seed order (neighbouring threads walk
+    neighbouring elements); results do not depend on it."""
     L = _lib.lib()
-    seed = to_device(seed, torch.int64)
+    seed = to_device(seed if isinstance(seed, torch.Tensor) else np.asarray(seed, np.int64),
+                     torch.int64)
     nt = int(seed.shape[0])
     counts = torch.empty(nt, dtype=torch.int64, device=seed.device)
-    args = (ptr(seed), nt, ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris), topo.ne,
+    order = torch.argsort(seed) if (sort_by_seed and nt > 1) else None
+    args = (ptr(seed), nt, ptr(order), ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris), topo.ne,
             int(layers), int(bool(centroids)))
     check(L.fm_patch_count(*args, ptr(counts), _stream()), "fm_patch_count")
     offsets = torch.zeros(nt + 1, dtype=torch.int64, device=seed.device)

@@ -83,6 +83,9 @@ def main():
         res[f"nnz_{key}"] = int(off[-1])
         if not cen:
             off_v, idx_v = off, idx
+            ms_u, _ = timed(lambda: D.patch_supports(topo, seed_d, a.layers, cen,
+                                                     sort_by_seed=False))
+            res["patch_vertices_unsorted_ms"] = ms_u
     # patch fit, degree 2, unit weights, scalar field (fm_fit_many)
     src = D.to_device(coords)
     f = D.to_device(np.sin(coords[:, 0]) * np.cos(coords[:, 1]) + 2)
