@@ -481,18 +481,22 @@ class PatchTopology:
                    tris.to(torch.int32).contiguous(), ne)
 
 
-def patch_supports(topo, seed, layers, centroids, sort_by_seed=True):
+def patch_supports(topo, seed, layers, centroids, sort_by_seed=None):
     """ElementPatch support CSR on the device (fm_patch_count / fm_patch_fill;
     pointwise.py:212-230): (offsets int64 (nt+1), idx int64, counts int64 (nt),
     -1 where a patch exceeds FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS).
-    Targets are processed in seed order (neighbouring threads walk
-    neighbouring elements); results do not depend on it."""
+    Vertex-dof patches process targets in seed order (neighbouring threads
+    walk neighbouring elements; measured 0.58 -> 0.50 ms at 1M random seeds
+    including the sort); centroid patches are cheap enough that the sort does
+    not pay (sort_by_seed=None picks this).  Results do not depend on it."""
     L = _lib.lib()
     seed = to_device(seed if isinstance(seed, torch.Tensor) else np.asarray(seed, np.int64),
                      torch.int64)
     nt = int(seed.shape[0])
     counts = torch.empty(nt, dtype=torch.int64, device=seed.device)
-    order = torch.argsort(seed) if (sort_by_seed and nt > 1) else None
+    if sort_by_seed is None:
+        sort_by_seed = not centroids
+    order = torch.argsort(seed.to(torch.int32)) if (sort_by_seed and nt > 1) else None
     args = (ptr(seed), nt, ptr(order), ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris), topo.ne,
             int(layers), int(bool(centroids)))
     check(L.fm_patch_count(*args, ptr(counts), _stream()), "fm_patch_count")

@@ -86,6 +86,7 @@ def main():
             ms_u, _ = timed(lambda: D.patch_supports(topo, seed_d, a.layers, cen,
                                                      sort_by_seed=False))
             res["patch_vertices_unsorted_ms"] = ms_u
+            res["seed_argsort_ms"], _ = timed(lambda: torch.argsort(seed_d.to(torch.int32)))
     # patch fit, degree 2, unit weights, scalar field (fm_fit_many)
     src = D.to_device(coords)
     f = D.to_device(np.sin(coords[:, 0]) * np.cos(coords[:, 1]) + 2)
