@@ -8,6 +8,7 @@ compute calls raise.
 """
 
 from . import errors
+from .cycle import PointwiseCycle
 from .locate import PointGrid, build_point_grid
 from .pointwise import (
     AdaptiveRadius,
@@ -32,6 +33,7 @@ kernel_backend = "b200"
 __all__ = [
     "errors",
     "PointGrid",
+    "PointwiseCycle",
     "build_point_grid",
     "AdaptiveRadius",
     "ElementPatch",

@@ -292,7 +292,46 @@ def patch_cases():
     save("patch", **out)
 
 
+def cycle_cases():
+    """metrics._PointwiseCycle (metrics.py:127-148): fields after 1 and 3
+    vertex -> centroid -> vertex cycles on one mesh, and after 2 cycles
+    between two meshes, for a radius selection and an element patch."""
+    from fieldbridge.metrics import _PointwiseCycle
+    from fieldbridge.pointwise import (AdaptiveRadius, ElementPatch, FitSpec, RadialBasisSpec,
+                                       RbfKind)
+
+    m, m2 = fb.square(12), fb.square(9)
+    out = {}
+    for name, mm in (("a", m), ("b", m2)):
+        for k in ("coords", "tris", "edge_tris", "tri_xy", "tri_edges", "vert_gid", "tri_gid",
+                  "inv2a", "epsfac", "diameters", "bbox"):
+            out[f"{name}_{k}"] = getattr(mm, k)
+        out[f"{name}_centroids"] = mm.centroids()
+    f0 = np.sin(m.coords[:, 0]) * np.cos(m.coords[:, 1]) + 2
+    out["f0"] = f0
+    out["mean_edge_length"] = np.float64(m.mean_edge_length)
+    specs = {
+        "adaptive": FitSpec(2, RadialBasisSpec(RbfKind.C4, a=2.0),
+                            AdaptiveRadius(12, m.mean_edge_length, 1.5)),
+        "patch": FitSpec(1, RadialBasisSpec(RbfKind.CONST, r_c=None), ElementPatch(2)),
+    }
+    for key, spec in specs.items():
+        cyc = _PointwiseCycle(m, spec, None)
+        v = f0
+        for it in range(1, 4):
+            v = cyc.cycle(v)
+            if it in (1, 3):
+                out[f"{key}_one_{it}"] = v
+        cyc2 = _PointwiseCycle(m, spec, m2)
+        v = f0
+        for it in range(2):
+            v = cyc2.cycle(v)
+        out[f"{key}_two_2"] = v
+    save("cycle", **out)
+
+
 if __name__ == "__main__":
+    cycle_cases()
     patch_cases()
     locate_cases()
     rbf_table()
