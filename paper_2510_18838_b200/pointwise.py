@@ -17,8 +17,7 @@ Differences that are not extensions:
     results are the reference's threads=1 results).
   * ElementPatch selection runs on the device:
     element grid, fm_locate_batch, fm_patch_count/fill, fm_fit_many; a patch
-    beyond FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS raises FieldmapError, and
-    transfer_extrinsic with ElementPatch raises NotImplementedError.
+    beyond FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS raises FieldmapError.
 """
 
 import enum
@@ -657,8 +656,8 @@ def transfer_extrinsic(evaluate_callback, target_points, fitspec, source_points,
     targets = _as_points(target_points, src_xy.shape[1])
     nt = targets.shape[0]
     if _check_patch(fitspec, mesh):
-        raise NotImplementedError("transfer_extrinsic with ElementPatch selection is not on "
-                                  "the B200 path (SURVEY.md §8(f) rank 3)")
+        return _transfer_extrinsic_patch(evaluate_callback, targets, fitspec, src_xy,
+                                         batch_size, mesh, source_location)
     cloud = D.SourceCloud(src_xy)
     grid = _GridHandle(cloud)
     out = np.empty(nt, dtype=np.float64)
@@ -687,6 +686,37 @@ def transfer_extrinsic(evaluate_callback, target_points, fitspec, source_points,
         if int(stats[0].item()) > 0:
             plan.raise_fit_error(status, b0)
         out[b0:b1] = vals.cpu().numpy()
+    return out
+
+
+def _transfer_extrinsic_patch(evaluate_callback, targets, fitspec, src_xy, batch_size, mesh,
+                              source_location):
+    """transfer_extrinsic's batch loop (pointwise.py:488-510) with ElementPatch
+    selection: per batch, locate + patch supports on the device, one callback
+    for the batch's distinct dofs, the fit on the device."""
+    from .locate import ElementGrid
+
+    nt = targets.shape[0]
+    eg = ElementGrid(mesh)
+    out = np.empty(nt, dtype=np.float64)
+    values_cache = np.full(src_xy.shape[0], np.nan, dtype=np.float64)
+    for bi, b0 in enumerate(range(0, nt, batch_size)):
+        b1 = min(b0 + batch_size, nt)
+        chunk = targets[b0:b1]
+        ps = _PatchSupports(chunk, fitspec, mesh, source_location, eg, base_index=b0)
+        needed = torch.unique(ps.idx).cpu().numpy()
+        try:
+            got = np.asarray(evaluate_callback(src_xy[needed]), dtype=np.float64)
+        except Exception as exc:
+            raise ExtrinsicEvaluationError(
+                f"evaluation callback failed on batch {bi} "
+                f"(targets {b0}..{b1 - 1}): {exc}", batch=bi) from exc
+        if got.shape != (needed.size,):
+            raise ExtrinsicEvaluationError(
+                f"callback returned {got.shape} values for {needed.size} "
+                f"points on batch {bi}", batch=bi)
+        values_cache[needed] = got
+        out[b0:b1] = ps.values(src_xy, values_cache).cpu().numpy()
     return out
 
 

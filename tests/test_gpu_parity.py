@@ -841,3 +841,31 @@ def test_pointwise_cycle_vs_reference(key):
     assert dv.is_cuda and np.array_equal(dv.cpu().numpy(), fin)
     cyc2 = PointwiseCycle(a, spec, target_mesh=b)
     np.testing.assert_allclose(cyc2.iterate(d["f0"], 2), d[f"{key}_two_2"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("loc", ["vertices", "centroids"])
+def test_transfer_extrinsic_element_patch(loc):
+    """transfer_extrinsic with ElementPatch (pointwise.py:467-510): a callback
+    returning the field's own dof values reproduces the intrinsic path
+    bitwise (reference test_pointwise.py:254-271) and the reference's values;
+    one callback per batch."""
+    d = golden("patch")
+    mesh = _golden_mesh(d, "sq")
+    src = d["sq_coords"] if loc == "vertices" else d["sq_centroids"]
+    t = d["sq_targets"]
+    f = np.sin(src[:, 0]) * np.cos(src[:, 1]) + 2
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.CONST, r_c=None), P.ElementPatch(3))
+    calls = []
+
+    def cb(pts):
+        calls.append(pts.shape[0])
+        key = {tuple(p): i for i, p in enumerate(src)}
+        return f[[key[tuple(p)] for p in pts]]
+
+    got = P.transfer_extrinsic(cb, t, spec, src, batch_size=128, mesh=mesh,
+                               source_location=loc)
+    intr = P.fit_point_cloud(src, f, t, spec, mesh=mesh, source_location=loc)
+    assert len(calls) == -(-t.shape[0] // 128)
+    assert np.array_equal(got, intr)
+    np.testing.assert_allclose(got, d[f"sq_{loc}_fit_2_3"], rtol=1e-10, atol=0)
