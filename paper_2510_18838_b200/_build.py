@@ -31,8 +31,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
 
 def _deps_hash(src):
     h = hashlib.sha1()
-    for p in [src] + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [
-            os.path.join(ROOT, "include", "fieldmap.h")]:
+    for p in [src] + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(
+            glob.glob(os.path.join(ROOT, "include", "*.h"))):
         with open(p, "rb") as f:
             h.update(f.read())
     h.update(" ".join(ARCH + FLAGS).encode())
