@@ -238,7 +238,7 @@ def b200_step(src_d, tgt_d, X_d, spec, marks):
     mark("build")
     Y = op.apply(X_d)
     mark("apply")
-    return Y, op, cnt, stats
+    return Y, op, cnt, stats, cloud
 
 
 def run_b200(args, rank, world, local_rank):
@@ -256,19 +256,20 @@ def run_b200(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def step(marks):
-        Y, op, cnt, stats = b200_step(src_d, tgt_d, X_d, spec, marks)
+        Y, op, cnt, stats, cloud = b200_step(src_d, tgt_d, X_d, spec, marks)
+        Yl = Y
         if world > 1:
             Y = gather_target_field(Y, nt_local * world)
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             marks.append(("allgather", e))
-        return Y, op, cnt, stats
+        return Y, op, cnt, stats, (cloud, Yl)
 
     sampler = ClockSampler(local_rank)
     with sampler:
         sampler.wait_first_sample()
         for _ in range(args.warmup):
-            Y, op, cnt, stats = step([])
+            Y, op, cnt, stats, extra = step([])
         torch.cuda.synchronize()
         if int(stats[0].item()) != 0:
             raise SystemExit(f"{int(stats[0].item())} fits failed in the benchmark workload")
@@ -281,7 +282,7 @@ def run_b200(args, rank, world, local_rank):
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             marks = []
-            Y, op, cnt, stats = step(marks)
+            Y, op, cnt, stats, extra = step(marks)
             torch.cuda.synchronize()
             for (a, ea), (b, eb) in zip(marks[:-1], marks[1:]):
                 phase[b] = phase.get(b, 0.0) + ea.elapsed_time(eb)
@@ -318,11 +319,16 @@ def run_b200(args, rank, world, local_rank):
             if world > 1:
                 # sharded public API: this rank's rows, then the NCCL all-gather
                 # of the full target field, then D2H
+                # of the full target field on every device; each rank's host
+                # reads back its own rows (the field is complete across the
+                # ranks' hosts -- copying all of it to every host would cost
+                # N x the PCIe traffic for the same data)
                 Yd = P.fit_point_cloud(src_h, X_h.to("cuda", non_blocking=True), tgt_h, spec)
                 Yf = gather_target_field(Yd, nt_local * world)
-                Yh = torch.empty(Yf.shape, dtype=Yf.dtype, pin_memory=True)
-                Yh.copy_(Yf, non_blocking=True)
+                Yh = torch.empty(Yd.shape, dtype=Yd.dtype, pin_memory=True)
+                Yh.copy_(Yd, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
+                del Yf
                 return Yh.numpy()
             # one-shot transfer of the 8-component field (pointwise.py:434):
             # host pinned buffers in, pinned host result out
@@ -350,12 +356,15 @@ def run_b200(args, rank, world, local_rank):
         e2e_s = float(te.item())
         e2e = {"value": nt_local * world * args.steps / e2e_s, "unit": "targets/s",
                "h2d_bytes_per_step": int(src.nbytes + tgt.nbytes + X.nbytes),
-               "d2h_bytes_per_step": int(nt_local * world * C * 8),
+               "d2h_bytes_per_step": int(nt_local * C * 8),
                "ms_per_step": 1e3 * e2e_s / args.steps}
 
     if rank != 0:
         return None
     cpu = None if (args.no_cpu or world > 1) else cpu_baseline(args, src, tgt, X, spec)
+    par = None
+    if not args.no_parity and world == 1:
+        par = parity_block(src, tgt, X, spec, extra[0], tgt_d, cnt, op, extra[1])
     line = {
         "metric": METRIC,
         "value": value,
@@ -368,10 +377,10 @@ def run_b200(args, rank, world, local_rank):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (reference mesh generators restated bitwise; fields sin((c+1)x)cos(y)+2)",
-        "config": dict(desc, parallelism=f"target-sharded x{world}" + (
+        "data": DATA,
+        "config": bench_config(desc, world),
+        "parallelism": f"target-sharded x{world}" + (
             " + NCCL all-gather of the target field" if world > 1 else ""),
-            l2="flushed between timed steps (256 MiB write)"),
         "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
         "gpu_launches": launches_per_step(cnt) * args.steps,
         "roofline": {
@@ -403,6 +412,7 @@ def run_b200(args, rank, world, local_rank):
         "nnz": op.nnz,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": par,
         "clocks": sampler.summary(),
     }
     return line
@@ -413,7 +423,10 @@ _REF = {}  # state shared with forked workers (set before the fork, never pickle
 
 
 def _ref_chunk(bounds):
-    """Worker: the reference's compiled kernels on one target chunk."""
+    """Worker: the reference's compiled kernels (oracle/_ref) on one chunk of
+    the sampled targets -- PreparedTransfer's selection + weights
+    (pointwise.py:233-296) and one fit_many per component (its apply
+    re-solves per call, pointwise.py:418-431)."""
     b0, b1 = bounds
     st = _REF
     from oracle import ref
@@ -422,86 +435,198 @@ def _ref_chunk(bounds):
     g, spec, X, src = st["grid"], st["spec"], st["X"], st["src"]
     sel = spec.selection
     tg = st["tg"][b0:b1]
-    off, idx, dist, radii, status = E.adaptive_radius_supports(
-        tg, g.points, float(g.lo[0]), float(g.lo[1]), g.dx, g.dy, g.nx, g.ny, g.cell_offsets,
-        g.cell_items, sel.min_points, sel.r0, sel.growth, st["r_max"])
-    w = np.empty(idx.shape[0])
-    for i in range(tg.shape[0]):  # pointwise.py:266-269 (per-target weight loop)
-        w[off[i]:off[i + 1]] = E.rbf_weights(st["kind"], spec.rbf.a, float(radii[i]),
-                                             dist[off[i]:off[i + 1]])
+    if hasattr(sel, "min_points"):
+        off, idx, dist, radii, status = E.adaptive_radius_supports(
+            tg, g.points, float(g.lo[0]), float(g.lo[1]), g.dx, g.dy, g.nx, g.ny,
+            g.cell_offsets, g.cell_items, sel.min_points, sel.r0, sel.growth, st["r_max"])
+        w = np.empty(idx.shape[0])
+        for i in range(tg.shape[0]):  # pointwise.py:266-269 (per-target weight loop)
+            w[off[i]:off[i + 1]] = E.rbf_weights(st["kind"], spec.rbf.a, float(radii[i]),
+                                                 dist[off[i]:off[i + 1]])
+    else:
+        off, idx, dist = E.fixed_radius_supports(
+            tg, g.points, float(g.lo[0]), float(g.lo[1]), g.dx, g.dy, g.nx, g.ny,
+            g.cell_offsets, g.cell_items, sel.r_c)
+        w = E.rbf_weights(st["kind"], spec.rbf.a, sel.r_c, dist)  # pointwise.py:250
     w = np.abs(w)  # pointwise.py:301
     out = np.empty((tg.shape[0], X.shape[1]))
-    for c in range(X.shape[1]):  # PreparedTransfer.apply re-solves per component
+    for c in range(X.shape[1]):
         v, _c, _st = E.fit_many(tg, off, idx, w, src, st["Xc"][c], spec.degree, spec.lam,
                                 spec.centering)
         out[:, c] = v
-    return out
+    return b0, out
 
 
-def reference_sample(src, tgt, X, spec, nsample, procs):
-    """Time the reference CPU path on `nsample` targets with `procs` processes:
-    PointGrid build (restated, oracle/pointgrid.py) + the reference's compiled
-    adaptive_radius_supports / rbf_weights / fit_many (oracle/_ref) per chunk."""
-    import multiprocessing as mp
+class ReferenceCPU:
+    """The reference CPU path on all host cores: one persistent fork pool
+    (OPENBLAS_NUM_THREADS=1 per worker), targets in chunks.  Each step maps a
+    uniform-stride sample of the WHOLE target set (every `stride`-th target,
+    so the graded disk's cheap and expensive regions are both represented)
+    and rebuilds the source PointGrid (locate.py:144-161, restated in
+    oracle/pointgrid.py) -- the grid's time is charged at the sample's share
+    of the full target set, because one grid serves all targets."""
 
-    from oracle.oracle import r_max_for
-    from oracle.pointgrid import OraclePointGrid
-    from paper_2510_18838_b200.pointwise import _KIND_CODE
+    def __init__(self, src, tgt, X, spec, stride, procs=None):
+        import multiprocessing as mp
 
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    t0 = time.perf_counter()
-    _REF.update(grid=OraclePointGrid(src), r_max=r_max_for(src, tgt), spec=spec, X=X, src=src,
-                tg=np.ascontiguousarray(tgt[:nsample]), kind=_KIND_CODE[spec.rbf.kind],
-                Xc=[np.ascontiguousarray(X[:, c]) for c in range(X.shape[1])])
-    bounds = np.linspace(0, nsample, procs + 1).astype(int)
-    work = [(int(b0), int(b1)) for b0, b1 in zip(bounds[:-1], bounds[1:])]
-    if procs > 1:
-        with mp.get_context("fork").Pool(procs) as pool:
-            parts = pool.map(_ref_chunk, work)
-    else:
-        parts = [_ref_chunk(w) for w in work]
-    dt = time.perf_counter() - t0
-    return np.concatenate(parts), dt
+        from oracle.oracle import r_max_for
+        from oracle.pointgrid import OraclePointGrid
+        from paper_2510_18838_b200.pointwise import _KIND_CODE
+
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        self.procs = procs or (os.cpu_count() or 1)
+        self.src, self.nt, self.stride = src, tgt.shape[0], max(1, int(stride))
+        self.sample = np.ascontiguousarray(tgt[::self.stride])
+        self.ns = self.sample.shape[0]
+        _REF.update(grid=OraclePointGrid(src), r_max=r_max_for(src, tgt), spec=spec, X=X,
+                    src=src, tg=self.sample, kind=_KIND_CODE[spec.rbf.kind],
+                    Xc=[np.ascontiguousarray(X[:, c]) for c in range(X.shape[1])])
+        nchunks = 8 * self.procs  # small chunks: load balance across the disk
+        b = np.linspace(0, self.ns, nchunks + 1).astype(int)
+        self.work = [(int(b0), int(b1)) for b0, b1 in zip(b[:-1], b[1:]) if b1 > b0]
+        self.pool = mp.get_context("fork").Pool(self.procs) if self.procs > 1 else None
+
+    def step(self):
+        """Returns (seconds charged to the sample, values of the sample)."""
+        from oracle.pointgrid import OraclePointGrid
+
+        t0 = time.perf_counter()
+        OraclePointGrid(self.src)  # the grid build of this transfer
+        t_grid = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        if self.pool is not None:
+            parts = self.pool.map(_ref_chunk, self.work, chunksize=1)
+        else:
+            parts = [_ref_chunk(w) for w in self.work]
+        t_map = time.perf_counter() - t1
+        out = np.concatenate([p for _, p in sorted(parts, key=lambda x: x[0])])
+        return t_grid * self.ns / self.nt + t_map, out
+
+    def describe(self):
+        return (f"every {self.stride}-th of the {self.nt} targets ({self.ns} targets, all "
+                f"components) per step on {self.procs} forked processes (one persistent pool, "
+                f"OPENBLAS_NUM_THREADS=1); source PointGrid rebuilt each step and charged at "
+                f"{self.ns}/{self.nt} of its time; reference kernels = oracle/_ref (the "
+                f"reference's _ext.pyx compiled with its own flags)")
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
 
 
-def cpu_baseline(args, src, tgt, X, spec, procs=None):
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def ref_stride(nt, procs):
+    """Sample stride: about 25k targets per host process per step (a few
+    seconds of CPU), never more than the whole set."""
+    return max(1, int(math.ceil(nt / (25000.0 * max(1, procs)))))
+
+
+def cpu_baseline(args, src, tgt, X, spec):
     from oracle import ref
 
     if not ref.available():
         return {"unavailable": "oracle/_ref not built"}
-    procs = procs or (os.cpu_count() or 1)
-    nsample = min(tgt.shape[0], 2000 * procs)
-    _, dt = reference_sample(src, tgt, X, spec, nsample, procs)
-    return {"value": nsample / dt, "unit": "targets/s", "cores": procs, "kind": "reference",
-            "sample": f"first {nsample} targets of the workload, all {X.shape[1]} components, "
-                      f"{procs} processes; PointGrid of all sources rebuilt per run"}
+    procs = os.cpu_count() or 1
+    rc = ReferenceCPU(src, tgt, X, spec, ref_stride(tgt.shape[0], procs), procs)
+    try:
+        dt, _ = rc.step()
+    finally:
+        rc.close()
+    return {"value": rc.ns / dt, "unit": "targets/s", "cores": procs, "kind": "reference",
+            "cpu_model": cpu_model(), "sample": rc.describe()}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return None
+    from oracle import ref
+
     src, tgt, X, spec, desc = workload(args.config, 0)
+    if not ref.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref (the reference's compiled "
+                "_ext.pyx) is not built"}
     procs = os.cpu_count() or 1
-    nsample = min(tgt.shape[0], 2000 * procs)
-    for _ in range(args.warmup):
-        reference_sample(src, tgt, X, spec, min(nsample, 4 * procs), procs)
-    total = 0.0
-    for _ in range(args.steps):
-        _, dt = reference_sample(src, tgt, X, spec, nsample, procs)
-        total += dt
-    value = nsample * args.steps / total
+    rc = ReferenceCPU(src, tgt, X, spec, ref_stride(tgt.shape[0], procs), procs)
+    try:
+        for _ in range(args.warmup):
+            rc.step()
+        total = 0.0
+        for _ in range(args.steps):
+            dt, _ = rc.step()
+            total += dt
+    finally:
+        rc.close()
+    value = rc.ns * args.steps / total
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "targets/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(desc, parallelism=f"{procs} host processes"),
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": bench_config(desc, world),
         "cpu_baseline": {"value": value, "unit": "targets/s", "cores": procs,
-                         "kind": "reference",
-                         "sample": f"first {nsample} targets of the workload per step"},
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "sample": rc.describe()},
         "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+
+
+# ---------------------------------------------------------------- parity
+def parity_block(src, tgt, X, spec, cloud, tgt_d, sel, op, Y):
+    """The benchmarked workload checked against the CPU oracle (outside the
+    timed region): neighbour CSR / radii / status bitwise, fit status equal,
+    values <= 1e-10 relative (oracle/parity.py)."""
+    from oracle import parity
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200.pointwise import _KIND_CODE
+
+    off, idx, dist, _w = D.support_csr(cloud, tgt_d, sel)
+    dev = {"off": off.cpu().numpy(), "idx": idx.cpu().numpy(), "dist": dist.cpu().numpy(),
+           "values": Y.cpu().numpy(), "fit_status": op.status.cpu().numpy()}
+    s = spec.selection
+    if hasattr(s, "min_points"):
+        dev["radii"] = sel.radii.cpu().numpy()
+        dev["status"] = sel.status.cpu().numpy()
+        osel = ("adaptive", s.min_points, s.r0, s.growth)
+    else:
+        osel = ("fixed", s.r_c)
+    return parity.check_transfer(src, X, tgt, spec.degree, _KIND_CODE[spec.rbf.kind],
+                                 spec.rbf.a, osel, dev, spec.lam, spec.centering)
+
+
+DATA = "synthetic (reference mesh generators restated bitwise; fields sin((c+1)x)cos(y)+2)"
+
+
+def bench_config(desc, world):
+    """The `config` object -- identical for both arms."""
+    return dict(desc, n_gpus=world, l2="flushed between timed steps (256 MiB write)")
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: run N ranks under
+    torch.distributed.run on this node (127.0.0.1) and pass rank 0's line
+    through."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -513,7 +638,10 @@ def main():
     ap.add_argument("--config", choices=["c1", "c2", "lattice1m"], default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

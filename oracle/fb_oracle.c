@@ -84,6 +84,16 @@ int orc_rbf(int kind, double a, double r_c, const double *r, int64_t n, double *
     return 0;
 }
 
+/* pointwise.py:266-269: rbf_weights of each target's support at that
+ * target's own final radius (the adaptive per-target loop, in C). */
+int orc_rbf_per_target(int kind, double a, const int64_t *off, int64_t nt,
+                       const double *radii, const double *r, double *out) {
+    if (kind < 0 || kind > 7) return -1;
+    for (int64_t t = 0; t < nt; t++)
+        for (int64_t j = off[t]; j < off[t + 1]; j++) out[j] = rbf_one(kind, a, radii[t], r[j]);
+    return 0;
+}
+
 /* ----------------------------------------------------------------- grid */
 typedef struct {
     int dim;

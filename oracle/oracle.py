@@ -230,11 +230,14 @@ def rbf_for_supports(kind, a, off, dist, radius):
         return np.ones_like(dist)
     if np.ndim(radius) == 0:
         return rbf_weights(kind, a, float(radius), dist)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    dist = np.ascontiguousarray(dist, dtype=np.float64)
+    radius = np.ascontiguousarray(radius, dtype=np.float64)
     w = np.empty_like(dist)
-    for i in range(off.shape[0] - 1):
-        lo, hi = off[i], off[i + 1]
-        if hi > lo:
-            w[lo:hi] = rbf_weights(kind, a, float(radius[i]), dist[lo:hi])
+    if kind < 0 or kind > 7:
+        raise ValueError(f"unknown rbf kind code {kind}")
+    lib().orc_rbf_per_target(ctypes.c_int(kind), ctypes.c_double(a), _p(off),
+                             _i64(off.shape[0] - 1), _p(radius), _p(dist), _p(w))
     return w
 
 

@@ -1,0 +1,104 @@
+"""Parity at benchmark scale (-m gpu): the benchmarked C2 workload and a
+2M-point random Gaussian / multiquadric transfer, end to end on the device,
+against the CPU oracle on all host cores (oracle/parity.py).
+
+Bars (north_star): neighbour CSR (offsets, ids, distances), adaptive radii
+and selection status bit-exact; fit status equal; every value of every
+component within 1e-10 relative of the oracle (the oracle restates
+_ext.pyx and is pinned bitwise to the reference in test_oracle.py).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from oracle import parity
+from paper_2510_18838_b200 import device as D
+from paper_2510_18838_b200 import pointwise as P
+from paper_2510_18838_b200 import synth
+from paper_2510_18838_b200.pointwise import _KIND_CODE
+
+pytestmark = pytest.mark.gpu
+
+VALUE_RTOL = 1e-10
+C2_H = 0.001956233500370731  # synth.disk_graded(1, 577, 0.6).mean_edge_length
+
+
+def _device_run(src, X, tgt, spec, slot_cap=None):
+    """The device path (grid -> order -> select -> operator -> apply) with the
+    reference-format support CSR read back for the comparison."""
+    src_d, tgt_d = D.to_device(src), D.to_device(tgt)
+    cloud = D.SourceCloud(src)
+    perm = cloud.target_order(tgt_d)
+    s = spec.selection
+    if isinstance(s, P.AdaptiveRadius):
+        dsel = D.adaptive(s.min_points, s.r0, s.growth, P._r_max(src, tgt))
+        osel = ("adaptive", s.min_points, s.r0, s.growth)
+    else:
+        dsel = D.fixed(s.r_c)
+        osel = ("fixed", s.r_c)
+    sl = D.select(cloud, tgt_d, dsel, perm, 0, slot_cap=slot_cap)
+    op, _stats = D.build_operator(cloud, tgt_d, sl, P._rbf_pair(spec.rbf), spec.degree,
+                                  spec.lam, spec.centering)
+    Y = op.apply(D.to_device(X))
+    off, idx, dist, _w = D.support_csr(cloud, tgt_d, sl)
+    dev = {"off": off.cpu().numpy(), "idx": idx.cpu().numpy(), "dist": dist.cpu().numpy(),
+           "values": Y.cpu().numpy(), "fit_status": op.status.cpu().numpy()}
+    if sl.radii is not None:
+        dev["radii"] = sl.radii.cpu().numpy()
+        dev["status"] = sl.status.cpu().numpy()
+    del src_d
+    return dev, osel, sl
+
+
+def _assert_parity(r):
+    assert r["supports_bitwise"], r
+    assert r.get("radii_bitwise", True), r
+    assert r.get("select_status_equal", True), r
+    assert r["fit_status_equal"], r
+    assert r["max_rel"] <= VALUE_RTOL, r
+
+
+def test_c2_full_scale_vs_oracle():
+    """BASELINE configs[1] exactly as bench.py runs it: 1,000,519 graded-disk
+    sources -> 1,000,519 uniform-disk targets, adaptive radius, C4, degree 2,
+    8 components.  The select pass's guessed first scan, its list overflow
+    restart and the rescan after a wide scan all occur on this input."""
+    src = synth.disk_graded(1.0, 577, 0.6).coords
+    tgt = synth.disk(1.0, 577).coords
+    X = synth.sincos_field(src, 8)
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.AdaptiveRadius(12, C2_H, 1.5))
+    dev, osel, sl = _device_run(src, X, tgt, spec)
+    r = parity.check_transfer(src, X, tgt, 2, O.RBF_C4, 2.0, osel, dev, rtol=VALUE_RTOL)
+    print(r)
+    assert r["nnz"] == 17478625
+    _assert_parity(r)
+
+
+@pytest.mark.parametrize("slot_cap", [None, 24])
+def test_random_2m_gaussian_multiquadric_vs_oracle(slot_cap):
+    """C3 at 2M: random sources/targets, AdaptiveRadius(12, 1.5/sqrt(N), 1.5),
+    Gaussian and multiquadric (a=2), degree 2.  Supports reach ~60; with
+    slot_cap=24 every support above 24 (about a third) overflows its slot and
+    goes through the build's re-gathering path at scale."""
+    n = 2_000_000
+    src = np.random.RandomState(1).uniform(0, 1, (n, 2))
+    tgt = np.random.RandomState(2).uniform(0, 1, (n, 2))
+    X = np.sin(src[:, :1]) * np.cos(src[:, 1:]) + 2.0
+    ref = None
+    for kind in (P.RbfKind.GAUSSIAN, P.RbfKind.MULTIQUADRIC):
+        spec = P.FitSpec(2, P.RadialBasisSpec(kind, a=2.0),
+                         P.AdaptiveRadius(12, 1.5 / math.sqrt(n), 1.5))
+        dev, osel, sl = _device_run(src, X, tgt, spec, slot_cap)
+        if slot_cap is not None:
+            assert sl.n_overflow > 0.2 * n
+        ref = parity.oracle_transfer(src, X, tgt, 2, _KIND_CODE[kind], 2.0, osel)
+        r = parity.check_transfer(src, X, tgt, 2, _KIND_CODE[kind], 2.0, osel, dev,
+                                  rtol=VALUE_RTOL, ref=ref)
+        print(kind, r)
+        assert np.diff(dev["off"]).max() >= 48
+        _assert_parity(r)
+        torch.cuda.empty_cache()
