@@ -190,7 +190,9 @@ int fm_fit_many(const fm_fit *fit, const double *targets, int64_t nt, const int6
  * in discovery order; fm_support_fill gives the id-sorted CSR of
  * _sort_by_id, _ext.pyx:155-169) into a fixed-stride slot buffer indexed by
  * PROCESSING POSITION k (the k-th entry of perm):
- * slot_id/slot_pos[k*slot_cap + i] = source id / index into sorted_pts.
+ * slot_pos[k*slot_cap + i] = index into sorted_pts (and, when slot_id is
+ * not NULL, slot_id[k*slot_cap + i] = its source id; the build does not
+ * need it: it reads ids as sorted_ids[slot_pos]).
  * counts/radii/status are indexed by target and equal fm_support_count's.
  * Adaptive selection evaluates several radii of the reference's growth
  * sequence per window scan (first scan at a density-guessed step) -- the
@@ -230,7 +232,7 @@ int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, in
  * launches once per non-empty bucket; without it once over every position. */
 typedef struct fm_lists {
     const int32_t *counts;
-    const int32_t *slot_id;
+    const int32_t *slot_id;     /* unused by the build (ids = sorted_ids[slot_pos]); may be NULL */
     const int32_t *slot_pos;
     int32_t slot_cap;
     int32_t n_overflow;

@@ -320,7 +320,7 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
     if (!fit_ok(fit)) return fit && fit->degree <= 3 ? FM_ERR_UNSUPPORTED : FM_ERR_ARG;
     if (fit->dim != grid->dim || rbf->kind < 0 || rbf->kind > 7) return FM_ERR_ARG;
     if (sel->adaptive && !radii) return FM_ERR_ARG;
-    if (lists && (!lists->counts || !lists->slot_id || !lists->slot_pos || lists->slot_cap < 1 ||
+    if (lists && (!lists->counts || !lists->slot_pos || lists->slot_cap < 1 ||
                   lists->n_overflow < 0 || (lists->n_overflow > 0 && !lists->overflow) ||
                   (lists->bucket_list && lists->bucket_stride < nt)))
         return FM_ERR_ARG;
@@ -343,7 +343,6 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
     b.stats = stats;
     int rc;
     if (lists) {
-        b.slot_id = lists->slot_id;
         b.slot_pos = lists->slot_pos;
         b.slot_cap = lists->slot_cap;
         b.counts = lists->counts;

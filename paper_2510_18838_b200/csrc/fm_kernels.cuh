@@ -10,6 +10,9 @@
 #include "fm_fit.cuh"
 #include "fm_search.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace fm {
 
 constexpr int kBlock = 128;
@@ -218,7 +221,6 @@ __global__ void __launch_bounds__(kBlock) k_support_fill(SearchArgs s, const int
 struct BuildArgs {
     const int32_t *klist;  // positions to process, or null for 0..nk-1
     int64_t nk;
-    const int32_t *slot_id;
     const int32_t *slot_pos;
     int slot_cap;
     const int32_t *counts;  // support size per target (FROM_SLOTS)
@@ -246,7 +248,7 @@ struct TileIn {
     int64_t k;
     PosInfo pi;
     double t[DIM];
-    int32_t ids[ROWS], spos[ROWS];
+    int32_t spos[ROWS];
     int64_t off;
 };
 
@@ -263,12 +265,8 @@ __device__ __forceinline__ void fetch_tile(const BuildArgs &b, int64_t ii, int64
 #pragma unroll
     for (int q = 0; q < ROWS; q++) {
         const int i = q * G + glane;
-        T.ids[q] = 0;
         T.spos[q] = 0;
-        if (i < b.slot_cap) {
-            T.ids[q] = __ldg(b.slot_id + k * b.slot_cap + i);
-            T.spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
-        }
+        if (i < b.slot_cap) T.spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
     }
     T.off = (!SOLVE && act) ? __ldg(b.offsets + k) : 0;
 }
@@ -281,11 +279,14 @@ __device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &
                                           const GroupSmem<G> &gs, int lane, int glane,
                                           bool active, int64_t k, int64_t tid,
                                           const double (&t)[DIM], double r, int m,
-                                          const int32_t (&ids)[ROWS],
                                           const int32_t (&spos)[ROWS], int64_t off, int &nfail,
                                           int &first_fail) {
     constexpr int K = Monos<DIM, DEG>::K;
     bool valid[ROWS];
+    int32_t ids[ROWS];  // source ids of the support rows (col of the operator)
+#pragma unroll
+    for (int q = 0; q < ROWS; q++)
+        ids[q] = q * G + glane < m ? __ldg(s.sorted_ids + spos[q]) : 0;
     double p[ROWS][DIM], w[ROWS], f[ROWS];
     const double inv_r = active ? 1.0 / r : 0.0;
 #pragma unroll
@@ -374,8 +375,8 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
                 m = 0;
             }
             build_one<DIM, DEG, G, ROWS, SOLVE>(s, b, gs, lane, glane, active, cur.k, cur.pi.tid,
-                                                cur.t, cur.pi.r, m, cur.ids, cur.spos, cur.off,
-                                                nfail, first_fail);
+                                                cur.t, cur.pi.r, m, cur.spos, cur.off, nfail,
+                                                first_fail);
             cur = nxt;
         }
     } else {
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
             load_target<DIM>(s.targets, tid, active, t);
             const double r = active ? (s.radii ? s.radii[tid] : s.sel.r_c) : 0.0;
             int m = 0;
-            int32_t ids[ROWS], spos[ROWS];
+            int32_t spos[ROWS];
             if (FROM_SLOTS) {
                 m = active ? b.counts[tid] : 0;
                 if (m > b.slot_cap) {  // overflow: built by the rescan launch
@@ -398,7 +399,6 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
 #pragma unroll
                 for (int q = 0; q < ROWS; q++) {
                     const int i = q * G + glane;
-                    ids[q] = i < m ? __ldg(b.slot_id + k * b.slot_cap + i) : 0;
                     spos[q] = i < m ? __ldg(b.slot_pos + k * b.slot_cap + i) : 0;
                 }
             } else {
@@ -409,13 +409,12 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
 #pragma unroll
                 for (int q = 0; q < ROWS; q++) {
                     const int i = q * G + glane;
-                    ids[q] = i < m ? gs.sid[i] : 0;
                     spos[q] = i < m ? gs.spos[i] : 0;
                 }
             }
             const int64_t off = (!SOLVE && active) ? b.offsets[k] : 0;
             build_one<DIM, DEG, G, ROWS, SOLVE>(s, b, gs, lane, glane, active, k, tid, t, r, m,
-                                                ids, spos, off, nfail, first_fail);
+                                                spos, off, nfail, first_fail);
         }
     }
     if (b.stats) warp_flush_pair(b.stats, nfail, first_fail);
@@ -474,10 +473,9 @@ __global__ void __launch_bounds__(kBlock, G == 8 ? 8 : 1) k_select(SearchArgs s,
             if (listed && m <= slot_cap) {
                 // supports in discovery order (the fit does not need id order;
                 // the reference-format CSR is sorted by fm_support_fill)
-                int32_t *oid = slot_id + k * slot_cap;
                 int32_t *opos = slot_pos + k * slot_cap;
                 for (int e = glane; e < m; e += G) {
-                    oid[e] = lb.id[e];
+                    if (slot_id) slot_id[k * slot_cap + e] = lb.id[e];
                     opos[e] = lb.pos[e];
                 }
             } else if (glane == 0) {
@@ -506,6 +504,102 @@ __global__ void __launch_bounds__(kBlock, G == 8 ? 8 : 1) k_select(SearchArgs s,
                     nshort++;
                     first_short = min(first_short, (int)tid);
                 }
+            }
+        }
+        __syncwarp();
+    }
+    local_max = __reduce_max_sync(FM_FULL_MASK, local_max);
+    local_min = __reduce_min_sync(FM_FULL_MASK, (unsigned)local_min);
+    if (lane == 0) {
+        atomicMax(stats + 0, local_max);
+        atomicMin(stats + 1, local_min);
+    }
+    warp_flush_pair(stats + 2, nshort, first_short);
+    warp_flush_pair(stats + 4, nstat, first_stat);
+}
+
+// Thread-per-target select pass (1-D / 2-D): same outputs as k_select.
+// The supports go from the per-thread shared-memory lists to the slots with
+// one coalesced warp store per target (lanes over entries).
+constexpr int kThreadListCap = 48;  // 8 CTAs/SM: 8 x 25 KB of lists
+
+template <int DIM>
+__global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t min_required, int lcap,
+                                                     int32_t *__restrict__ counts,
+                                                     double *__restrict__ radii,
+                                                     uint8_t *__restrict__ status,
+                                                     int32_t *__restrict__ slot_id,
+                                                     int32_t *__restrict__ slot_pos, int slot_cap,
+                                                     int32_t *__restrict__ overflow,
+                                                     int32_t *__restrict__ stats,
+                                                     PosInfo *__restrict__ pos_info,
+                                                     double *__restrict__ pos_t) {
+    extern __shared__ __align__(16) char smem[];
+    const int stride = lcap | 1;  // odd: a warp's appends spread over the banks
+    int32_t *lpos_all = reinterpret_cast<int32_t *>(smem);
+    __shared__ RadiusTable tab;
+    fill_radius_table(tab, s.sel);
+    ThreadList L;
+    L.e = lpos_all + threadIdx.x * stride;
+    L.cap = lcap;
+    const int lane = threadIdx.x & 31;
+    const int wbase = threadIdx.x & ~31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    int local_max = 0, local_min = INT32_MAX;
+    int nshort = 0, first_short = INT32_MAX, nstat = 0, first_stat = INT32_MAX;
+    for (int64_t tile = warp; tile * 32 < s.nt; tile += nwarps) {
+        const int64_t k = tile * 32 + lane;
+        const bool active = k < s.nt;
+        int m = 0;
+        bool slotted = false;
+        if (active) {
+            const int64_t tid = s.perm ? (int64_t)__ldg(s.perm + k) : k;
+            double t[DIM];
+            load_target<DIM>(s.targets, tid, true, t);
+            double r;
+            uint8_t st;
+            bool listed;
+            m = select_thread<DIM>(s.g, s.cell_start, s.sorted_pts, t, s.sel, tab, L, r, st,
+                                   listed);
+            slotted = listed && m <= slot_cap;
+            if (!slotted) overflow[atomicAdd(stats + 6, 1)] = (int32_t)k;
+            if (pos_info) pos_info[k] = make_pos_info((int32_t)tid, m, s.sel.adaptive ? r : s.sel.r_c);
+            if (pos_t) {
+#pragma unroll
+                for (int a = 0; a < DIM; a++) pos_t[k * DIM + a] = t[a];
+            }
+            counts[tid] = m;
+            if (s.sel.adaptive) {
+                if (radii) radii[tid] = r;
+                if (status) status[tid] = st;
+                if (st) {
+                    nstat++;
+                    first_stat = min(first_stat, (int)tid);
+                }
+            }
+            local_max = max(local_max, m);
+            local_min = min(local_min, m);
+            if (m < min_required) {
+                nshort++;
+                first_short = min(first_short, (int)tid);
+            }
+        }
+        __syncwarp();
+        // supports -> slots: one target at a time, lanes over its entries
+        const int mine = slotted ? m : 0;
+        unsigned todo = __ballot_sync(FM_FULL_MASK, mine > 0);
+        while (todo) {
+            const int r = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int mr = __shfl_sync(FM_FULL_MASK, mine, r);
+            const int64_t kr = tile * 32 + r;
+            const int32_t *lp = lpos_all + (wbase + r) * stride;
+            int32_t *op = slot_pos + kr * slot_cap;
+            for (int e = lane; e < mr; e += 32) {
+                const int32_t p = lp[e] & kPosMask;
+                op[e] = p;
+                if (slot_id) slot_id[kr * slot_cap + e] = __ldg(s.sorted_ids + p);
             }
         }
         __syncwarp();
@@ -664,6 +758,15 @@ int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *i
     return FM_OK;
 }
 
+// FM_SELECT_GROUPS=1 forces the lane-group select in 1-D/2-D (A/B checks)
+inline bool select_groups_forced() {
+    static const int v = [] {
+        const char *e = getenv("FM_SELECT_GROUPS");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 // per-group candidate list of the select pass (at least slot_cap): 64 keeps
 // 8 CTAs/SM within shared memory for the 2-D slots
 constexpr int kSelectListCap = 64;
@@ -673,11 +776,25 @@ int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, do
                   uint8_t *status, int32_t *slot_id, int32_t *slot_pos, int slot_cap,
                   int32_t *overflow, int32_t *stats, PosInfo *pos_info, double *pos_t,
                   cudaStream_t st) {
-    // 8-lane groups in 1-D/2-D (small windows: 4 targets per warp halves the
-    // per-target fixed cost), 16 lanes for the larger windows of dim >= 3
+    // 1-D/2-D: one thread per target (k_select_t); dim >= 3: 16-lane groups
+    // (windows of many rows)
     constexpr int G = DIM <= 2 ? 8 : 16;
     k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0);
     if (s.nt == 0) return FM_OK;
+    if (DIM <= 2 && !select_groups_forced()) {
+        const int lcap = slot_cap < kThreadListCap ? slot_cap : kThreadListCap;
+        const size_t sm = (size_t)kBlock * (lcap | 1) * sizeof(int32_t);
+        if (sm > 48 * 1024)
+            cudaFuncSetAttribute(k_select_t<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        const int64_t tiles = (s.nt + 31) / 32;
+        const int blocks = (int)std::min<int64_t>((tiles + 3) / 4, (int64_t)kSMs * 8);
+        k_select_t<DIM><<<blocks, kBlock, sm, st>>>(s, min_required, lcap, counts, radii, status,
+                                                    slot_id, slot_pos, slot_cap, overflow, stats,
+                                                    pos_info, pos_t);
+        FM_CHECK_LAUNCH();
+        return FM_OK;
+    }
     const int lcap = slot_cap > kSelectListCap ? slot_cap : kSelectListCap;
     const size_t per = ((size_t)lcap * 16 + sizeof(RowTable<G>) + 15) & ~(size_t)15;
     const size_t sm = per * (kBlock / G);

@@ -562,4 +562,223 @@ __device__ __forceinline__ int select_target(const GridDev &g, const int32_t *__
     return m;
 }
 
+// ======================================================================
+// Thread-per-target selection (1-D / 2-D)
+// ======================================================================
+// One thread owns one target and walks its window rows sequentially; the
+// kept candidates go to a per-thread list in shared memory (source grid
+// position + "level", the index of the first radius of the sequence whose
+// threshold the candidate passes).  Compared with the lane-group scan this
+// removes the per-candidate ballots, prefix sums and row-table cursor walks
+// (the group select issued ~370 warp instructions per target on C2).
+// Exactness is unchanged: the same conservative row clipping as Window, the
+// same d^2 < T(r) test against the same thresholds.
+
+// Per-thread list in shared memory: entry e of thread i at i*stride + e
+// (stride odd: appends of a warp spread over the banks; a cooperative read
+// of one thread's list is contiguous).  An entry is the candidate's source
+// grid position (< 2^30) with a 2-bit code in bits 30-31: the number of the
+// two lower thresholds of the scan (T[j-2], T[j-1]) that its d^2 reaches.
+struct ThreadList {
+    int32_t *e;
+    int cap;
+};
+constexpr int kCodeShift = 30;
+constexpr int32_t kPosMask = (1 << kCodeShift) - 1;
+
+// One window scan of target t at radius r with thresholds thr_hi = T(r) and
+// two lower ones thr_mid <= thr_hi, thr_lo <= thr_mid (0: unused): appends
+// every candidate with d^2 < thr_hi (entries beyond cap are counted, not
+// stored).  Returns the kept count; c_mid / c_lo receive #{d^2 < thr_mid},
+// #{d^2 < thr_lo}.
+template <int DIM>
+__device__ __forceinline__ int scan_thread(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                           const double *__restrict__ sorted_pts, const double *t,
+                                           double r, double thr_hi, double thr_mid, double thr_lo,
+                                           ThreadList &L, int &c_mid, int &c_lo) {
+    const double rs = r * (1.0 + kSlackRel);
+    const double rs2 = rs * rs;
+    const double eps_r2 = 8.0 * 2.220446049250313e-16 * rs2;
+    int32_t clo[kMaxDim], span[kMaxDim];
+    int64_t stride[kMaxDim];
+    int32_t nrows = 1;
+    int64_t st = 1;
+#pragma unroll
+    for (int a = 0; a < DIM; a++) {
+        clo[a] = (int32_t)cell_of(t[a] - rs, g.lo[a], g.inv_d[a], g.n[a]);
+        span[a] = (int32_t)cell_of(t[a] + rs, g.lo[a], g.inv_d[a], g.n[a]) - clo[a] + 1;
+        stride[a] = st;
+        st *= g.n[a];
+        if (a > 0) nrows *= span[a];
+    }
+    int n = 0, nm = 0, nl = 0;
+    auto visit = [&](int32_t p, double d2) {
+        if (d2 < thr_hi) {
+            const int code = (d2 >= thr_mid ? 1 : 0) + (d2 >= thr_lo ? 1 : 0);
+            nm += d2 < thr_mid;
+            nl += d2 < thr_lo;
+            if (n < L.cap) L.e[n] = p | (code << kCodeShift);
+            n++;
+        }
+    };
+    for (int32_t row = 0; row < nrows; row++) {
+        int32_t rem = row;
+        int64_t base = 0;
+        double off2 = 0.0;
+#pragma unroll
+        for (int a = 1; a < DIM; a++) {
+            int64_t ia;
+            if (a == DIM - 1) {
+                ia = clo[a] + rem;
+            } else {
+                ia = clo[a] + rem % span[a];
+                rem /= span[a];
+            }
+            base += ia * stride[a];
+            const double d = g.d[a];
+            const double blo = ia == 0 ? -INFINITY : g.lo[a] + (double)ia * d;
+            const double bhi = ia == g.n[a] - 1 ? INFINITY : g.lo[a] + (double)(ia + 1) * d;
+            const double slack = 8.0 * 2.220446049250313e-16 *
+                                     (fabs(g.lo[a]) + fabs(t[a]) + (double)(ia + 1) * d) +
+                                 kSlackRel * d;
+            double gap = fmax(blo - t[a], t[a] - bhi) - slack;
+            gap = fmax(gap, 0.0);
+            off2 += gap * gap;
+        }
+        const double hw2 = rs2 - off2;
+        if (!(hw2 >= -eps_r2)) continue;
+        const double hw = sqrt(fmax(hw2, 0.0) + eps_r2) * (1.0 + kSlackRel);
+        const int64_t x0 = cell_of(t[0] - hw, g.lo[0], g.inv_d[0], g.n[0]);
+        const int64_t x1 = cell_of(t[0] + hw, g.lo[0], g.inv_d[0], g.n[0]);
+        const int32_t p0 = __ldg(cell_start + base + x0);
+        const int32_t p1 = __ldg(cell_start + base + x1 + 1);
+        int32_t p = p0;
+        for (; p + 1 < p1; p += 2) {  // two point loads in flight
+            double pa[DIM], pb[DIM];
+            load_point<DIM>(sorted_pts, p, pa);
+            load_point<DIM>(sorted_pts, p + 1, pb);
+            visit(p, dist2_rn<DIM>(pa, t));
+            visit(p + 1, dist2_rn<DIM>(pb, t));
+        }
+        if (p < p1) {
+            double pa[DIM];
+            load_point<DIM>(sorted_pts, p, pa);
+            visit(p, dist2_rn<DIM>(pa, t));
+        }
+    }
+    c_mid = nm;
+    c_lo = nl;
+    return n;
+}
+
+// Density guess of the growth step for one thread (2-D; see guess_steps).
+template <int DIM>
+__device__ __forceinline__ int guess_steps_thread(const GridDev &g,
+                                                  const int32_t *__restrict__ cell_start,
+                                                  const double *t, const fm_select &sel) {
+    if (DIM != 2) return 0;
+    const int64_t nx = g.n[0], ny = g.n[1];
+    const int64_t cx = cell_of(t[0], g.lo[0], g.inv_d[0], nx);
+    const int64_t cy = cell_of(t[1], g.lo[1], g.inv_d[1], ny);
+    const int64_t x0 = cx > 0 ? cx - 1 : 0, x1 = cx + 1 < nx ? cx + 1 : nx - 1;
+    const int64_t y0 = cy > 0 ? cy - 1 : 0, y1 = cy + 1 < ny ? cy + 1 : ny - 1;
+    int n = 0;
+    for (int64_t y = y0; y <= y1; y++)
+        n += __ldg(cell_start + y * nx + x1 + 1) - __ldg(cell_start + y * nx + x0);
+    const double area = (double)((x1 - x0 + 1) * (y1 - y0 + 1)) * g.d[0] * g.d[1];
+    const float r2_est = (float)((double)sel.min_pts * area /
+                                 (3.14159265f * (n > 0 ? (float)n : 0.5f)));
+    float r = (float)sel.r0, g2 = (float)sel.growth;
+    int k = 0;
+    while (k < kMaxGuess && r * r < r2_est) {
+        r *= g2;
+        k++;
+    }
+    return k;
+}
+
+// Final support of one target (thread version of select_target): returns m;
+// on return the list holds exactly the m supports (discovery order, code
+// bits cleared) when `listed`, otherwise m > L.cap.
+//
+// Adaptive: ONE scan at the density-guessed step kg (exact for 82% of the C2
+// targets, one too high for 14%) counts the sequence's radii kg-2, kg-1, kg at
+// once; the first of them holding min_pts is the reference's radius unless
+// the count at kg-2 already suffices (then: restart at r0) or the count at kg
+// does not (then: continue the sequence one scan per radius, _ext.pyx:258-271).
+template <int DIM>
+__device__ __forceinline__ int select_thread(const GridDev &g, const int32_t *__restrict__ cell_start,
+                                             const double *__restrict__ sorted_pts, const double *t,
+                                             const fm_select &sel, const RadiusTable &tab,
+                                             ThreadList &L, double &r_out, uint8_t &status,
+                                             bool &listed) {
+    status = 0;
+    int kg = 0;
+    if (sel.adaptive) {
+        kg = guess_steps_thread<DIM>(g, cell_start, t, sel);
+        int j = 0;
+        while (j < kg && tab.r[j] < sel.r_max && j + 1 < kRadTab) j++;
+        kg = j;
+    }
+    const double t_mid = kg >= 1 ? tab.thr[kg - 1] : 0.0;
+    const double t_lo = kg >= 2 ? tab.thr[kg - 2] : 0.0;
+    int c_mid, c_lo;
+    int n = scan_thread<DIM>(g, cell_start, sorted_pts, t, tab.r[kg], tab.thr[kg], t_mid, t_lo,
+                             L, c_mid, c_lo);
+    int jf = -1, m = n;
+    bool exact_list = false;
+    if (!sel.adaptive) {
+        jf = 0;
+        exact_list = true;
+    } else if (c_lo >= sel.min_pts) {
+        jf = -1;  // the guess was at least two steps high: restart at r0
+    } else if (c_mid >= sel.min_pts) {
+        jf = kg - 1;
+        m = c_mid;
+    } else if (n >= sel.min_pts) {
+        jf = kg;
+        exact_list = true;
+    } else if (tab.r[kg] >= sel.r_max) {  // r_max reached short (_ext.pyx:266)
+        jf = kg;
+        status = 1;
+        exact_list = true;
+    } else {
+        jf = -2;  // continue the sequence
+    }
+    if (jf < 0) {
+        int j = jf == -1 ? 0 : kg + 1;
+        for (;;) {
+            double r, thr;
+            seq_radius(tab, sel, j, r, thr);
+            int cm, cl;
+            m = scan_thread<DIM>(g, cell_start, sorted_pts, t, r, thr, 0.0, 0.0, L, cm, cl);
+            if (m >= sel.min_pts) break;
+            if (r >= sel.r_max) {
+                status = 1;
+                break;
+            }
+            j++;
+        }
+        jf = j;
+        n = m;
+        exact_list = true;
+    }
+    double rf, thr_f;
+    seq_radius(tab, sel, jf, rf, thr_f);
+    r_out = sel.adaptive ? rf : sel.r_c;
+    listed = m <= L.cap;
+    if (!listed) return m;
+    if (!exact_list && n > L.cap) {  // the wider scan overflowed the list; the support fits
+        int cm, cl;
+        scan_thread<DIM>(g, cell_start, sorted_pts, t, rf, thr_f, 0.0, 0.0, L, cm, cl);
+    } else if (!exact_list) {  // jf = kg - 1: keep codes 0 and 1 (d^2 < T[kg-1])
+        int c = 0;
+        for (int e = 0; e < n; e++) {
+            const uint32_t v = (uint32_t)L.e[e];
+            if ((v >> kCodeShift) <= 1u) L.e[c++] = (int32_t)v;
+        }
+    }
+    return m;
+}
+
 }  // namespace fm

@@ -255,7 +255,7 @@ class Selection:
     counts: torch.Tensor    # int32 (nt,) by target
     radii: torch.Tensor     # f64 (nt,) final radius (adaptive) or None
     status: torch.Tensor    # u8 (nt,) adaptive status or None
-    slot_id: torch.Tensor   # int32 (nt * slot_cap,) by processing position
+    slot_id: torch.Tensor   # int32 (nt * slot_cap,) by processing position, or None
     slot_pos: torch.Tensor
     slot_cap: int
     overflow: torch.Tensor  # int32 positions whose support did not fit a slot
@@ -279,7 +279,9 @@ class Selection:
     def lists(self):
         nb = _lib.FM_NBUCKETS
         buckets = self.bucket_list is not None and self.bucket_count is not None
-        return FmLists(self.counts.data_ptr(), self.slot_id.data_ptr(), self.slot_pos.data_ptr(),
+        return FmLists(self.counts.data_ptr(),
+                       self.slot_id.data_ptr() if self.slot_id is not None else None,
+                       self.slot_pos.data_ptr(),
                        int(self.slot_cap), self.n_overflow, self.overflow.data_ptr(),
                        self.pos_info.data_ptr() if self.pos_info is not None else None,
                        self.pos_t.data_ptr() if self.pos_t is not None else None,
@@ -298,7 +300,7 @@ def select(cloud, targets, sel, perm=None, min_required=0, slot_cap=None):
     counts = _empty(nt, torch.int32, dev)
     radii = _empty(nt, torch.float64, dev) if sel.adaptive else None
     status = _empty(nt, torch.uint8, dev) if sel.adaptive else None
-    slot_id = _empty(max(nt * cap, 1), torch.int32, dev)
+    slot_id = None  # the build reads ids as sorted_ids[slot_pos]
     slot_pos = _empty(max(nt * cap, 1), torch.int32, dev)
     overflow = _empty(max(nt, 1), torch.int32, dev)
     pos_info = _empty(max(nt, 1) * 2, torch.float64, dev)  # 16 B records

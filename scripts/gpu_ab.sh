@@ -1,11 +1,15 @@
-# A/B timing of library variants: bash scripts/gpu_ab.sh TAG name1 name2 ...
-# ("base" = the in-tree libfieldmap.so; others = _lib/var/libfieldmap_NAME.so)
-TAG=$1; shift
+# A/B on the GPU: GPU tests, then the bench (device timing only) under each
+# environment setting given as arguments (e.g. "FM_SELECT_GROUPS=1").
+# usage: bash scripts/gpu_ab.sh TAG [ENV=VAL ...]
+TAG=${1:-ab}
+shift
 mkdir -p gpurun_out
-for v in "$@"; do
-  if [ "$v" = base ]; then unset FM_LIB_PATH; else export FM_LIB_PATH=$PWD/paper_2510_18838_b200/_lib/var/libfieldmap_$v.so; fi
-  for rep in 1 2; do
-    timeout 300 python bench.py --no-e2e --no-cpu > gpurun_out/ab_${TAG}_${v}_$rep.log 2>&1
-    echo "$v rep$rep rc=$? $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/ab_${TAG}_${v}_$rep.log) $(grep -o '"phases_ms_per_step": {[^}]*}' gpurun_out/ab_${TAG}_${v}_$rep.log)" >> gpurun_out/ab_$TAG.txt
-  done
+timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo pytest=$? >> gpurun_out/status_$TAG.txt
+timeout 300 python bench.py --no-e2e --no-cpu --no-parity > gpurun_out/bench_${TAG}_base.json 2>&1; echo bench=$? >> gpurun_out/status_$TAG.txt
+i=0
+for kv in "$@"; do
+  i=$((i+1))
+  env $kv timeout 300 python bench.py --no-e2e --no-cpu --no-parity > gpurun_out/bench_${TAG}_v$i.json 2>&1; echo "v$i($kv)=$?" >> gpurun_out/status_$TAG.txt
 done
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-parity"
+timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 ; echo launches=$? >> gpurun_out/status_$TAG.txt

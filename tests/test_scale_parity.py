@@ -82,7 +82,7 @@ def test_c2_full_scale_vs_oracle():
 def test_random_2m_gaussian_multiquadric_vs_oracle(slot_cap):
     """C3 at 2M: random sources/targets, AdaptiveRadius(12, 1.5/sqrt(N), 1.5),
     Gaussian and multiquadric (a=2), degree 2.  Supports reach ~60; with
-    slot_cap=24 every support above 24 (about a third) overflows its slot and
+    slot_cap=24 every support above 24 (about 12%) overflows its slot and
     goes through the build's re-gathering path at scale."""
     n = 2_000_000
     src = np.random.RandomState(1).uniform(0, 1, (n, 2))
@@ -94,7 +94,7 @@ def test_random_2m_gaussian_multiquadric_vs_oracle(slot_cap):
                          P.AdaptiveRadius(12, 1.5 / math.sqrt(n), 1.5))
         dev, osel, sl = _device_run(src, X, tgt, spec, slot_cap)
         if slot_cap is not None:
-            assert sl.n_overflow > 0.2 * n
+            assert sl.n_overflow > 0.05 * n
         ref = parity.oracle_transfer(src, X, tgt, 2, _KIND_CODE[kind], 2.0, osel)
         r = parity.check_transfer(src, X, tgt, 2, _KIND_CODE[kind], 2.0, osel, dev,
                                   rtol=VALUE_RTOL, ref=ref)
