@@ -124,6 +124,21 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
  * (device).  The `bbox` of locate.py:151. */
 int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t stream);
 
+/* Bounding boxes of two point arrays (b may be NULL with nb = 0) in one
+ * launch, returned to HOST memory (the call synchronises `stream`):
+ * lohi_host = [a.lo(dim), a.hi(dim), b.lo(dim), b.hi(dim)].  workspace:
+ * >= 32*dim bytes of device memory.  The bboxes of locate.py:151 and of
+ * pointwise.py:253-255 (r_max) with one device->host round trip. */
+int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t nb,
+                 double *lohi_host, void *workspace, fm_stream_t stream);
+
+/* Host-only: the PointGrid geometry for a source bbox -- _pad_bbox
+ * (locate.py:50-62) and _grid_shape (locate.py:34-47) for dim 2, cells of
+ * equal side for other dims -- as an fm_grid (lo/hi_out: padded box, may be
+ * NULL).  No device work. */
+int fm_grid_geometry(int dim, const double *bbox_lo, const double *bbox_hi, int64_t n_points,
+                     double cells_per_point, fm_grid *out, double *lo_out, double *hi_out);
+
 /* Processing order of targets for locality: the source grid's cells in
  * blocks of 8x8 (2-D), 4x4x4 (3-D) or 2^dim cells, block-major.  Results
  * never depend on it; perm[k] = target processed k-th. */

@@ -7,6 +7,8 @@
 // so the layout is deterministic, then the coordinates are gathered into cell
 // order so the radius search reads candidates with coalesced loads.
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 
 #include "fm_common.cuh"
 #include "fm_scan.cuh"
@@ -96,32 +98,56 @@ __global__ void k_scatter(const int32_t *__restrict__ keys, int64_t n,
     }
 }
 
-// ids ascending inside each cell (the lexsort tie order of locate.py:79)
-__global__ void k_sort_cells(const int32_t *__restrict__ start, int64_t ncell,
-                             int32_t *__restrict__ ids) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = start[c], e = start[c + 1];
-        for (int32_t i = b + 1; i < e; i++) {
-            const int32_t v = ids[i];
-            int32_t j = i - 1;
-            while (j >= b && ids[j] > v) {
-                ids[j + 1] = ids[j];
-                j--;
-            }
-            ids[j + 1] = v;
-        }
+// ids ascending inside each cell (the lexsort tie order of locate.py:79),
+// then the cell's coordinates gathered into cell order.  One thread per cell:
+// insertion sort for the usual handful of points, heapsort for crowded cells
+// (clustered or coincident sources) so the cost stays n log n.
+__device__ __forceinline__ void sift_down(int32_t *a, int32_t root, int32_t n) {
+    for (;;) {
+        int32_t c = 2 * root + 1;
+        if (c >= n) return;
+        if (c + 1 < n && a[c + 1] > a[c]) c++;
+        if (a[root] >= a[c]) return;
+        const int32_t t = a[root];
+        a[root] = a[c];
+        a[c] = t;
+        root = c;
     }
 }
 
 template <int DIM>
-__global__ void k_gather_pts(const int32_t *__restrict__ ids, int64_t n,
-                             const double *__restrict__ pts, double *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = ids[i];
+__global__ void k_sort_cells(const int32_t *__restrict__ start, int64_t ncell,
+                             int32_t *__restrict__ ids, const double *__restrict__ pts,
+                             double *__restrict__ sorted_pts) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = start[c], e = start[c + 1];
+        if (e - b <= 16) {
+            for (int32_t i = b + 1; i < e; i++) {
+                const int32_t v = ids[i];
+                int32_t j = i - 1;
+                while (j >= b && ids[j] > v) {
+                    ids[j + 1] = ids[j];
+                    j--;
+                }
+                ids[j + 1] = v;
+            }
+        } else {
+            int32_t *a = ids + b;
+            const int32_t n = e - b;
+            for (int32_t r = n / 2 - 1; r >= 0; r--) sift_down(a, r, n);
+            for (int32_t m = n - 1; m > 0; m--) {
+                const int32_t t = a[0];
+                a[0] = a[m];
+                a[m] = t;
+                sift_down(a, 0, m);
+            }
+        }
+        for (int32_t i = b; i < e; i++) {
+            const int64_t sidx = ids[i];
 #pragma unroll
-        for (int a = 0; a < DIM; a++) out[i * DIM + a] = pts[s * DIM + a];
+            for (int a = 0; a < DIM; a++) sorted_pts[(int64_t)i * DIM + a] = pts[sidx * DIM + a];
+        }
     }
 }
 
@@ -187,6 +213,58 @@ __global__ void k_bbox(const double *__restrict__ pts, int64_t n, unsigned long 
     }
 }
 
+// Boxes of up to two point arrays in one launch (blockIdx.y = array), for
+// fm_bbox_pair: keys accumulate with atomicMin only (the max as the
+// complement of its key), so one memset of 0xff initialises everything.
+template <int DIM>
+__global__ void k_bbox_pair(const double *__restrict__ a, int64_t na, const double *__restrict__ b,
+                            int64_t nb, unsigned long long *acc) {
+    const double *pts = blockIdx.y ? b : a;
+    const int64_t n = blockIdx.y ? nb : na;
+    unsigned long long *out = acc + blockIdx.y * 2 * DIM;
+    double mn[DIM], mx[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+        mn[k] = INFINITY;
+        mx[k] = -INFINITY;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < DIM; k++) {
+            const double v = pts[i * DIM + k];
+            mn[k] = fmin(mn[k], v);
+            mx[k] = fmax(mx[k], v);
+        }
+    }
+    __shared__ double s_mn[8][DIM], s_mx[8][DIM];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fmin(mn[k], __shfl_xor_sync(FM_FULL_MASK, mn[k], o));
+            mx[k] = fmax(mx[k], __shfl_xor_sync(FM_FULL_MASK, mx[k], o));
+        }
+        if (lane == 0) {
+            s_mn[wid][k] = mn[k];
+            s_mx[wid][k] = mx[k];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < DIM && n > 0) {
+        const int k = threadIdx.x;
+        double lo = s_mn[0][k], hi = s_mx[0][k];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+            lo = fmin(lo, s_mn[w][k]);
+            hi = fmax(hi, s_mx[w][k]);
+        }
+        if (lo <= hi) {
+            atomicMin(&out[k], dkey(lo));
+            atomicMin(&out[DIM + k], ~dkey(hi));
+        }
+    }
+}
+
 __global__ void k_bbox_final(const unsigned long long *acc, int dim, double *lohi) {
     const int a = threadIdx.x;
     if (a < 2 * dim) lohi[a] = dval(acc[a]);
@@ -201,16 +279,6 @@ static int launch_keys(const GridDev &g, const double *pts, int64_t n, int32_t *
         k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
     else if (blocks)
         k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
-    FM_CHECK_LAUNCH();
-    return FM_OK;
-}
-
-template <int DIM>
-static int launch_gather(const int32_t *ids, int64_t n, const double *pts, double *out,
-                         cudaStream_t s) {
-    const int threads = 256;
-    const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
-    if (blocks) k_gather_pts<DIM><<<(unsigned)blocks, threads, 0, s>>>(ids, n, pts, out);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -245,8 +313,7 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
     w += align256(sizeof(int32_t) * (size_t)ncell);
     void *scan_ws = w;
     const GridDev g = to_dev(grid);
-    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
-    cudaMemsetAsync(fill, 0, sizeof(int32_t) * (size_t)ncell, s);
+    cudaMemsetAsync(counts, 0, (size_t)((char *)(fill + ncell) - (char *)counts), s);
     int rc;
     switch (grid->dim) {
     case 1: rc = launch_keys<1>(g, pts, n, keys, counts, s); break;
@@ -265,17 +332,18 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
         k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, fill, sorted_ids);
     }
     {
-        const int64_t blocks = std::min<int64_t>((ncell + threads - 1) / threads, kSMs * 16);
-        k_sort_cells<<<(unsigned)blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids);
+        const unsigned blocks =
+            (unsigned)std::min<int64_t>((ncell + threads - 1) / threads, kSMs * 16);
+        switch (grid->dim) {
+        case 1: k_sort_cells<1><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        case 2: k_sort_cells<2><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        case 3: k_sort_cells<3><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        case 4: k_sort_cells<4><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        default: k_sort_cells<5><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        }
     }
     FM_CHECK_LAUNCH();
-    switch (grid->dim) {
-    case 1: return launch_gather<1>(sorted_ids, n, pts, sorted_pts, s);
-    case 2: return launch_gather<2>(sorted_ids, n, pts, sorted_pts, s);
-    case 3: return launch_gather<3>(sorted_ids, n, pts, sorted_pts, s);
-    case 4: return launch_gather<4>(sorted_ids, n, pts, sorted_pts, s);
-    default: return launch_gather<5>(sorted_ids, n, pts, sorted_pts, s);
-    }
+    return FM_OK;
 }
 
 int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t stream) {
@@ -326,8 +394,7 @@ int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int3
     w += align256(sizeof(int32_t) * (size_t)(ncell + 1));
     void *scan_ws = w;
     const GridDev g = to_dev(grid);
-    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
-    cudaMemsetAsync(fill, 0, sizeof(int32_t) * (size_t)ncell, s);
+    cudaMemsetAsync(counts, 0, (size_t)((char *)(fill + ncell) - (char *)counts), s);
     int rc;
     switch (grid->dim) {
     case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s, true); break;
@@ -346,6 +413,122 @@ int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int3
         k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, nt, start, fill, perm);
     }
     FM_CHECK_LAUNCH();
+    return FM_OK;
+}
+
+
+static double host_dval(unsigned long long k) {
+    const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    memcpy(&v, &b, sizeof v);
+    return v;
+}
+
+int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t nb,
+                 double *lohi_host, void *workspace, fm_stream_t stream) {
+    if (dim < 1 || dim > kMaxDim || na < 0 || nb < 0 || !lohi_host || !workspace)
+        return FM_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(workspace);
+    const size_t bytes = sizeof(unsigned long long) * 4 * (size_t)dim;
+    if (cudaMemsetAsync(acc, 0xff, bytes, s) != cudaSuccess) return FM_ERR_CUDA;
+    const int threads = 256;
+    const int64_t nmax = na > nb ? na : nb;
+    const unsigned bx =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>((nmax + threads - 1) / threads, kSMs * 4));
+    const dim3 grid(bx, nb > 0 ? 2 : 1);
+    switch (dim) {
+    case 1: k_bbox_pair<1><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
+    case 2: k_bbox_pair<2><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
+    case 3: k_bbox_pair<3><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
+    case 4: k_bbox_pair<4><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
+    default: k_bbox_pair<5><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
+    }
+    FM_CHECK_LAUNCH();
+    unsigned long long h[4 * kMaxDim];
+    if (cudaMemcpyAsync(h, acc, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return FM_ERR_CUDA;
+    for (int arr = 0; arr < 2; arr++)
+        for (int k = 0; k < dim; k++) {
+            lohi_host[arr * 2 * dim + k] = host_dval(h[arr * 2 * dim + k]);
+            lohi_host[arr * 2 * dim + dim + k] = host_dval(~h[arr * 2 * dim + dim + k]);
+        }
+    return FM_OK;
+}
+
+/* locate.py:50-62 (_pad_bbox) and 34-47 (_grid_shape) in C, for any dim
+ * (dim != 2: cells of equal side), bit for bit the Python grid_geometry(). */
+int fm_grid_geometry(int dim, const double *bbox_lo, const double *bbox_hi, int64_t n_points,
+                     double cells_per_point, fm_grid *out, double *lo_out, double *hi_out) {
+    if (dim < 1 || dim > kMaxDim || !out || !(cells_per_point > 0.0) || n_points < 0)
+        return FM_ERR_ARG;
+    double lo[kMaxDim], hi[kMaxDim];
+    double span = 0.0;
+    for (int k = 0; k < dim; k++) {
+        lo[k] = bbox_lo[k];
+        hi[k] = bbox_hi[k];
+        const double e = hi[k] - lo[k];
+        if (k == 0 || e > span) span = e;
+    }
+    span = span > 1.0 ? span : 1.0;  // max(float(np.max(hi - lo)), 1.0)
+    const double pad = 1e-12 * span;
+    for (int k = 0; k < dim; k++) {
+        if (hi[k] - lo[k] <= 0.0) {
+            const double h = 0.5 * (span > 1.0 ? span : 1.0);
+            lo[k] -= h;
+            hi[k] += h;
+        } else {
+            lo[k] -= pad;
+            hi[k] += pad;
+        }
+    }
+    int64_t shape[kMaxDim];
+    const double target = 1.0 > cells_per_point * (double)n_points ? 1.0
+                                                                    : cells_per_point * (double)n_points;
+    if (dim == 2) {
+        const double w = hi[0] - lo[0] > 0.0 ? hi[0] - lo[0] : 0.0;
+        const double h = hi[1] - lo[1] > 0.0 ? hi[1] - lo[1] : 0.0;
+        int64_t nx, ny;
+        if (w <= 0.0 && h <= 0.0) {
+            nx = ny = 1;
+        } else if (w <= 0.0) {
+            nx = 1;
+            ny = std::max<int64_t>(1, (int64_t)nearbyint(target));
+        } else if (h <= 0.0) {
+            nx = std::max<int64_t>(1, (int64_t)nearbyint(target));
+            ny = 1;
+        } else {
+            nx = std::max<int64_t>(1, (int64_t)nearbyint(sqrt(target * w / h)));
+            ny = std::max<int64_t>(1, (int64_t)nearbyint(target / (double)nx));
+        }
+        shape[0] = nx;
+        shape[1] = ny;
+    } else {
+        double prod = 1.0;
+        for (int k = 0; k < dim; k++) prod *= hi[k] - lo[k];
+        const double side = pow(prod / target, 1.0 / dim);
+        for (int k = 0; k < dim; k++)
+            shape[k] = std::max<int64_t>(1, (int64_t)nearbyint((hi[k] - lo[k]) / side));
+    }
+    memset(out, 0, sizeof *out);
+    out->dim = dim;
+    int64_t ncell = 1;
+    for (int k = 0; k < kMaxDim; k++) {
+        if (k < dim) {
+            out->n[k] = shape[k];
+            out->lo[k] = lo[k];
+            out->inv_d[k] = 1.0 / ((hi[k] - lo[k]) / (double)shape[k]);
+            ncell *= shape[k];
+            if (lo_out) lo_out[k] = lo[k];
+            if (hi_out) hi_out[k] = hi[k];
+        } else {
+            out->n[k] = 1;
+            out->lo[k] = 0.0;
+            out->inv_d[k] = 1.0;
+        }
+    }
+    out->ncell = ncell;
     return FM_OK;
 }
 

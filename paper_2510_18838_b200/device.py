@@ -21,8 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import FmFit, FmGrid, FmLists, FmRbf, FmSelect, check, ptr
-from .locate import grid_geometry
+from ._lib import FM_MAX_DIM, FmFit, FmGrid, FmLists, FmRbf, FmSelect, check, ptr
 
 INT32_MAX = 2 ** 31 - 1
 
@@ -70,22 +69,30 @@ class SourceCloud:
         if self.pts.ndim != 2 or not 1 <= self.pts.shape[1] <= 5 or self.pts.shape[0] == 0:
             raise ValueError("points must be a nonempty (n, d) array with 1 <= d <= 5")
         self.n, self.dim = self.pts.shape
+        L = _lib.lib()
         if geom is None:
             if bbox is None:
                 if host is not None:
                     bbox = (host.min(axis=0), host.max(axis=0))
                 else:
                     bbox = device_bbox(self.pts)
-            geom = grid_geometry(bbox[0], bbox[1], self.n, cells_per_point)
+            # the PointGrid geometry (locate.grid_geometry) computed in C
+            self.grid = FmGrid()
+            lo = np.ascontiguousarray(bbox[0], dtype=np.float64)
+            hi = np.ascontiguousarray(bbox[1], dtype=np.float64)
+            check(L.fm_grid_geometry(self.dim, lo.ctypes.data, hi.ctypes.data, self.n,
+                                     float(cells_per_point), ctypes.byref(self.grid), None, None),
+                  "fm_grid_geometry")
+        else:
+            self.grid = geom.to_ctypes()
         self.bbox = bbox  # exact (unpadded) source bbox on the host, or None
         self.geom = geom
-        self.grid = self.geom.to_ctypes()
+        ncell = int(self.grid.ncell)
         dev = self.pts.device
-        L = _lib.lib()
-        self.cell_start = _empty(self.geom.ncell + 1, torch.int32, dev)
+        self.cell_start = _empty(ncell + 1, torch.int32, dev)
         self.sorted_ids = _empty(self.n, torch.int32, dev)
         self.sorted_pts = _empty((self.n, self.dim), torch.float64, dev)
-        ws_bytes = L.fm_grid_workspace(self.n, self.geom.ncell)
+        ws_bytes = L.fm_grid_workspace(self.n, ncell)
         ws = _workspace(ws_bytes, dev)
         check(L.fm_grid_build(ctypes.byref(self.grid), ptr(self.pts), self.n,
                               ptr(self.cell_start), ptr(self.sorted_ids), ptr(self.sorted_pts),
@@ -109,14 +116,28 @@ def device_bbox(pts):
     return device_bboxes([pts])[0]
 
 
+_BBOX_WS = {}
+
+
 def device_bboxes(arrays):
-    """Bounding boxes of several device point arrays with ONE device->host sync."""
+    """Bounding boxes of one or two device point arrays: one launch and ONE
+    device->host round trip (fm_bbox_pair)."""
     dim = arrays[0].shape[1]
-    lohi = torch.empty((len(arrays), 2 * dim), dtype=torch.float64, device=arrays[0].device)
-    for i, pts in enumerate(arrays):
-        check(_lib.lib().fm_bbox(dim, ptr(pts), pts.shape[0], ptr(lohi[i]), _stream()), "fm_bbox")
-    h = lohi.cpu().numpy()
-    return [(h[i, :dim], h[i, dim:]) for i in range(len(arrays))]
+    if len(arrays) > 2:
+        return device_bboxes(arrays[:2]) + device_bboxes(arrays[2:])
+    dev = arrays[0].device
+    ws = _BBOX_WS.get(dev)
+    if ws is None:
+        ws = _BBOX_WS[dev] = torch.empty(64 * FM_MAX_DIM, dtype=torch.uint8, device=dev)
+    h = np.empty(4 * dim, dtype=np.float64)
+    a = arrays[0]
+    b = arrays[1] if len(arrays) > 1 else None
+    check(_lib.lib().fm_bbox_pair(dim, ptr(a), a.shape[0], ptr(b), 0 if b is None else b.shape[0],
+                                  h.ctypes.data, ptr(ws), _stream()), "fm_bbox_pair")
+    out = [(h[:dim].copy(), h[dim:2 * dim].copy())]
+    if b is not None:
+        out.append((h[2 * dim:3 * dim].copy(), h[3 * dim:].copy()))
+    return out
 
 
 # ------------------------------------------------------- selection spec
