@@ -7,7 +7,7 @@
 // c /= s^deg.  value = c[0] (centered) or mono(t) . c.
 //
 // B200 formulation.  One group of G lanes owns one target (G = 8 for k <= 6,
-// 16 for k <= 10, 32 up to k = 21: the rank test needs one lane per column);
+// 16 for k <= 10, 32 up to k = 21; 4 lanes for small 2-D supports);
 // lane l holds rows l, l+G, ... (ROWS per lane) of A in registers,
 // zero-padded -- a zero row changes neither R nor Q^T b.  The solve is an
 // unpivoted Householder QR with unnormalised reflectors v = x - beta e_j,
@@ -69,7 +69,7 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     constexpr Monos<DIM, DEG> M{};
     constexpr int K = Monos<DIM, DEG>::K;
     constexpr int NC = K + (SOLVE ? 1 : 0);
-    static_assert(G >= K, "the rank test assigns one lane per column");
+    static_assert(G * ROWS >= K, "a fit needs at least K row slots");
     const int gbase = lane & ~(G - 1);
     const bool centering = fp.centering != 0;
 
@@ -226,15 +226,19 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
     // the exact kappa only for warps where the bound cannot rule it out.
     bool singular = false;
     if (!ridge) {
+        // lane glane owns the columns l = glane, glane + G, ... (G may be < K)
         double offmax = 0.0, dmin = INFINITY, dmax = 0.0;
-        if (glane < K) {
-            const int l = glane;
-            const double d = fabs(sR[l * K + l]);
-            dmin = d;
-            dmax = d;
 #pragma unroll
-            for (int c = 1; c < K; c++)
-                if (c > l) offmax = fmax(offmax, fabs(sR[l * K + c]));
+        for (int l0 = 0; l0 < K; l0 += G) {
+            const int l = l0 + glane;
+            if (l < K) {
+                const double d = fabs(sR[l * K + l]);
+                dmin = fmin(dmin, d);
+                dmax = fmax(dmax, d);
+#pragma unroll
+                for (int c = 1; c < K; c++)
+                    if (c > l) offmax = fmax(offmax, fabs(sR[l * K + c]));
+            }
         }
         offmax = group_max<G>(offmax);
         dmax = group_max<G>(dmax);
@@ -247,19 +251,25 @@ __device__ __forceinline__ int fit_rows(const fm_fit &fp, const double *t, int m
         const bool unsure = !(bound < 1e12);  // NaN / inf / large: decide exactly
         if (__any_sync(FM_FULL_MASK, unsure)) {
             double colsum = 0.0, invsum = 0.0;
-            const int l = glane;
-            double x[K];
 #pragma unroll
-            for (int ii = 0; ii < K; ii++) {
-                const int i = K - 1 - ii;
-                double acc = (i == l) ? 1.0 : 0.0;
+            for (int l0 = 0; l0 < K; l0 += G) {
+                const int l = l0 + glane;
+                double cs = 0.0, is = 0.0;
+                double x[K];
 #pragma unroll
-                for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
-                x[i] = (i <= l) ? acc * sIb[i] : 0.0;
-                if (i <= l && l < K) {
-                    colsum += fabs(sR[i * K + l]);
-                    invsum += fabs(x[i]);
+                for (int ii = 0; ii < K; ii++) {
+                    const int i = K - 1 - ii;
+                    double acc = (i == l) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int c = i + 1; c < K; c++) acc = fma(-sR[i * K + c], x[c], acc);
+                    x[i] = (i <= l) ? acc * sIb[i] : 0.0;
+                    if (i <= l && l < K) {
+                        cs += fabs(sR[i * K + l]);
+                        is += fabs(x[i]);
+                    }
                 }
+                colsum = fmax(colsum, cs);
+                invsum = fmax(invsum, is);
             }
             const double kappa = group_max<G>(colsum) * group_max<G>(invsum);
             singular = unsure && !(kappa < kSingularKappa);

@@ -340,6 +340,7 @@ __device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
 __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MINB8_R2
                                           : (G == 8 && ROWS <= 4) ? FM_BUILD_MINB8
+                                          : (G == 4)              ? (ROWS <= 4 ? 4 : 3)
                                                                   : 1) k_build(SearchArgs s,
                                                                                  BuildArgs b) {
     constexpr int K = Monos<DIM, DEG>::K;
@@ -758,6 +759,16 @@ int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *i
     return FM_OK;
 }
 
+// Largest fit (rows) built with 4-lane groups; FM_BUILD_G4=<rows> overrides
+// (0 disables them; A/B checks)
+inline int build_g4_rows() {
+    static const int v = [] {
+        const char *e = getenv("FM_BUILD_G4");
+        return e ? atoi(e) : 24;
+    }();
+    return v;
+}
+
 // FM_SELECT_GROUPS=1 forces the lane-group select in 1-D/2-D (A/B checks)
 inline bool select_groups_forced() {
     static const int v = [] {
@@ -837,6 +848,15 @@ int launch_build(const SearchArgs &s, const BuildArgs &b, int max_m, cudaStream_
     if (b.nk == 0) return FM_OK;
     const int need = fit_rows_needed(max_m, K, b.fp.lam);
 #define FM_BUILD(GG, R) launch_build_rows<DIM, DEG, GG, R, SOLVE, FROM_SLOTS>(s, b, st)
+    // small supports of k <= 6 fits: 4-lane groups (8 targets per warp: a
+    // third of the butterfly levels and half the replicated scalar work of
+    // the 8-lane shape per target)
+    if constexpr (G0 == 8) {
+        const int g4 = build_g4_rows();
+        if (need <= 8 && need <= g4) return FM_BUILD(4, 2);
+        if (need <= 16 && need <= g4) return FM_BUILD(4, 4);
+        if (need <= 24 && need <= g4) return FM_BUILD(4, 6);
+    }
     if (need <= G0) return FM_BUILD(G0, 1);
     if (need <= 2 * G0) return FM_BUILD(G0, 2);
     if (need <= 3 * G0) return FM_BUILD(G0, 3);

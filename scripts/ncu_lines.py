@@ -3,8 +3,8 @@
 
     python scripts/ncu_lines.py REPORT KERNEL_REGEX [N] [--launch I]
 
-KERNEL_REGEX is matched against the FULL (demangled) kernel name, e.g.
-'k_build<2, 2, 8, 3' selects one size-bucket instantiation."""
+KERNEL_REGEX matches the kernel's base name (e.g. k_build); --launch I
+selects the I-th matching launch of the report (e.g. one size bucket)."""
 import csv
 import re
 import subprocess
@@ -13,7 +13,7 @@ import sys
 
 def lines(rep, regex, launch=None):
     args = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-            "-k", "regex:" + re.escape(regex) if "<" in regex else "regex:" + regex]
+            "-k", "regex:" + regex]
     if launch is not None:
         args += ["--launch-skip", str(launch), "--launch-count", "1"]
     out = subprocess.run(args, capture_output=True, text=True).stdout
@@ -46,7 +46,8 @@ def lines(rep, regex, launch=None):
 def main():
     rep, regex = sys.argv[1], sys.argv[2]
     n = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 25
-    agg = lines(rep, regex)
+    launch = int(sys.argv[sys.argv.index("--launch") + 1]) if "--launch" in sys.argv else None
+    agg = lines(rep, regex, launch)
     ts = sum(a[1] for a in agg.values()) or 1
     ti = sum(a[2] for a in agg.values()) or 1
     print(f"{regex}: {ti / 1e6:.1f}M warp instructions, {ts} stall samples")
