@@ -290,4 +290,28 @@ __device__ __forceinline__ unsigned group_bits(unsigned ballot, int lane) {
 
 __device__ __forceinline__ int warp_max_int(int v) { return __reduce_max_sync(FM_FULL_MASK, v); }
 
+// --------------------------------------------------- asynchronous copies
+// cp.async (global -> shared, bypassing registers); a false predicate
+// zero-fills the destination without reading the source.  Completion is per
+// thread: cp_async_wait_all() then __syncwarp() before other lanes read.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+                 "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+                 "r"(pred ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 }  // namespace fm

@@ -167,7 +167,7 @@ __device__ __forceinline__ GroupSmem<G> carve(char *base, int cap, int K) {
 }
 
 template <int G>
-inline size_t block_smem_bytes(int cap, int K) {
+__host__ __device__ inline size_t block_smem_bytes(int cap, int K) {
     return (size_t)(kBlock / G) * ((group_smem_bytes<G>(cap, K) + 15) & ~(size_t)15);
 }
 
@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kBlock) k_support_fill(SearchArgs s, const int
 // SOLVE: values[t] for the scalar field src_val.
 struct BuildArgs {
     const int32_t *klist;  // positions to process, or null for 0..nk-1
+    int stage;             // shared memory sized for the cp.async pipeline
     int64_t nk;
     const int32_t *slot_pos;
     int slot_cap;
@@ -239,55 +240,20 @@ struct BuildArgs {
     int32_t *stats;
 };
 
-// Inputs of one target of a build tile, staged one tile ahead on the slot
-// path (the dependent klist -> record/slots -> points chain is what the
-// build waits on; prefetching the next tile's records overlaps it with the
-// current tile's fit).
-template <int DIM, int ROWS>
-struct TileIn {
-    int64_t k;
-    PosInfo pi;
-    double t[DIM];
-    int32_t spos[ROWS];
-    int64_t off;
-};
-
-template <int DIM, int G, int ROWS, bool SOLVE>
-__device__ __forceinline__ void fetch_tile(const BuildArgs &b, int64_t ii, int64_t k, int glane,
-                                           TileIn<DIM, ROWS> &T) {
-    const bool act = ii < b.nk;
-    if (!act) k = 0;
-    T.k = k;
-    T.pi = act ? b.pos_info[k] : make_pos_info(0, 0, 0.0);
-#pragma unroll
-    for (int a = 0; a < DIM; a++) T.t[a] = act ? __ldg(b.pos_t + k * DIM + a) : 0.0;
-    // slot loads do not wait for m (in-bounds garbage past it is never used)
-#pragma unroll
-    for (int q = 0; q < ROWS; q++) {
-        const int i = q * G + glane;
-        T.spos[q] = 0;
-        if (i < b.slot_cap) T.spos[q] = __ldg(b.slot_pos + k * b.slot_cap + i);
-    }
-    T.off = (!SOLVE && act) ? __ldg(b.offsets + k) : 0;
-}
-
-// One target of the build: support rows -> weights -> fit -> operator row
-// (or value).  A function, not a lambda: a non-inlined lambda capturing the
-// kernel arguments by reference puts them in a local-memory stack frame.
+// One target of the build from its gathered support rows (coordinates p,
+// source ids): weights -> fit -> operator row (or value).  A function, not a
+// lambda: a non-inlined lambda capturing the kernel arguments by reference
+// puts them in a local-memory stack frame.
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
-__device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &b,
-                                          const GroupSmem<G> &gs, int lane, int glane,
-                                          bool active, int64_t k, int64_t tid,
-                                          const double (&t)[DIM], double r, int m,
-                                          const int32_t (&spos)[ROWS], int64_t off, int &nfail,
-                                          int &first_fail) {
+__device__ __forceinline__ void build_core(const BuildArgs &b, const GroupSmem<G> &gs, int lane,
+                                           int glane, bool active, int64_t tid,
+                                           const double (&t)[DIM], double r, int m,
+                                           const double (&p)[ROWS][DIM],
+                                           const int32_t (&ids)[ROWS], int64_t off, int &nfail,
+                                           int &first_fail) {
     constexpr int K = Monos<DIM, DEG>::K;
     bool valid[ROWS];
-    int32_t ids[ROWS];  // source ids of the support rows (col of the operator)
-#pragma unroll
-    for (int q = 0; q < ROWS; q++)
-        ids[q] = q * G + glane < m ? __ldg(s.sorted_ids + spos[q]) : 0;
-    double p[ROWS][DIM], w[ROWS], f[ROWS];
+    double w[ROWS], f[ROWS];
     const double inv_r = active ? 1.0 / r : 0.0;
 #pragma unroll
     for (int q = 0; q < ROWS; q++) {
@@ -295,10 +261,7 @@ __device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &
         valid[q] = i < m;
         w[q] = 0.0;
         f[q] = 0.0;
-#pragma unroll
-        for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
         if (valid[q]) {
-            load_point<DIM>(s.sorted_pts, spos[q], p[q]);
             const double d = __dsqrt_rn(dist2_rn<DIM>(p[q], t));
             w[q] = fabs(rbf_fast(b.rbf_kind, b.rbf_a, r, inv_r, d));  // pointwise.py:301
             if (SOLVE) f[q] = __ldg(b.src_val + ids[q]);
@@ -331,16 +294,111 @@ __device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &
     __syncwarp();
 }
 
+// build_core with the support rows gathered from global memory by grid position
+template <int DIM, int DEG, int G, int ROWS, bool SOLVE>
+__device__ __forceinline__ void build_one(const SearchArgs &s, const BuildArgs &b,
+                                          const GroupSmem<G> &gs, int lane, int glane,
+                                          bool active, int64_t k, int64_t tid,
+                                          const double (&t)[DIM], double r, int m,
+                                          const int32_t (&spos)[ROWS], int64_t off, int &nfail,
+                                          int &first_fail) {
+    int32_t ids[ROWS];  // source ids of the support rows (col of the operator)
+    double p[ROWS][DIM];
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const bool v = q * G + glane < m;
+        ids[q] = v ? __ldg(s.sorted_ids + spos[q]) : 0;
+#pragma unroll
+        for (int a = 0; a < DIM; a++) p[q][a] = 0.0;
+        if (v) load_point<DIM>(s.sorted_pts, spos[q], p[q]);
+    }
+    build_core<DIM, DEG, G, ROWS, SOLVE>(b, gs, lane, glane, active, tid, t, r, m, p, ids, off,
+                                         nfail, first_fail);
+}
+
+// ---------------------------------------------------- staged (cp.async) build
+// Per group, in shared memory: three record slots (the select pass's
+// position record, target coordinates, row offset, and the support's grid
+// positions) and two buffers of gathered support rows (coordinates, source
+// ids).  While tile n is fitted, tile n+1's support rows and tile n+2's
+// records are in flight as cp.async copies -- no registers held, no
+// dependent-load stalls in the fit.
+template <int DIM, int G, int ROWS>
+struct StageSmem {
+    struct __align__(16) Rec {
+        PosInfo pi;
+        double t[DIM];
+        int64_t off;
+    };
+    Rec rec[3];
+    int32_t spos[3][ROWS * G];
+    double pts[2][ROWS * G][DIM];
+    int32_t ids[2][ROWS * G];
+};
+
+template <int DIM, int G, int ROWS>
+__host__ __device__ constexpr size_t stage_bytes() {
+    return (sizeof(StageSmem<DIM, G, ROWS>) + 15) & ~(size_t)15;
+}
+
+// records + grid positions of position k (slot `sl`); inactive: zero record
+template <int DIM, int G, int ROWS, bool SOLVE>
+__device__ __forceinline__ void stage_records(const BuildArgs &b, StageSmem<DIM, G, ROWS> &S,
+                                              int sl, bool act, int64_t k, int glane) {
+    auto &R = S.rec[sl];
+    if (glane == 0) cp_async16(&R.pi, b.pos_info + k, act);
+    if (glane == (1 % G)) {
+        if (DIM == 2)
+            cp_async16(&R.t[0], b.pos_t + k * DIM, act);
+        else
+#pragma unroll
+            for (int a = 0; a < DIM; a++) cp_async8(&R.t[a], b.pos_t + k * DIM + a, act);
+    }
+    if (!SOLVE && glane == (2 % G)) cp_async8(&R.off, b.offsets + k, act);
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        cp_async4(&S.spos[sl][i], b.slot_pos + k * b.slot_cap + i, act && i < b.slot_cap);
+    }
+}
+
+// support rows (coordinates + ids) of the record in slot `sl` into buffer `pb`
+template <int DIM, int G, int ROWS>
+__device__ __forceinline__ void stage_rows(const SearchArgs &s, const BuildArgs &b,
+                                           StageSmem<DIM, G, ROWS> &S, int sl, int pb,
+                                           int glane) {
+    const int m = S.rec[sl].pi.m;
+    const bool fits = m <= b.slot_cap;
+#pragma unroll
+    for (int q = 0; q < ROWS; q++) {
+        const int i = q * G + glane;
+        const bool v = fits && i < m;
+        const int64_t sp = v ? S.spos[sl][i] : 0;
+        if (DIM == 2)
+            cp_async16(&S.pts[pb][i][0], s.sorted_pts + sp * DIM, v);
+        else
+#pragma unroll
+            for (int a = 0; a < DIM; a++) cp_async8(&S.pts[pb][i][a], s.sorted_pts + sp * DIM + a, v);
+        cp_async4(&S.ids[pb][i], s.sorted_ids + sp, v);
+    }
+}
+
 #ifndef FM_BUILD_MINB8
 #define FM_BUILD_MINB8 4
 #endif
 #ifndef FM_BUILD_MINB8_R2
 #define FM_BUILD_MINB8_R2 4
 #endif
+#ifndef FM_BUILD_MINB4
+#define FM_BUILD_MINB4 4
+#endif
+#ifndef FM_BUILD_MINB4_R6
+#define FM_BUILD_MINB4_R6 3
+#endif
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
 __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MINB8_R2
                                           : (G == 8 && ROWS <= 4) ? FM_BUILD_MINB8
-                                          : (G == 4)              ? (ROWS <= 4 ? 4 : 3)
+                                          : (G == 4)              ? (ROWS <= 4 ? FM_BUILD_MINB4 : FM_BUILD_MINB4_R6)
                                                                   : 1) k_build(SearchArgs s,
                                                                                  BuildArgs b) {
     constexpr int K = Monos<DIM, DEG>::K;
@@ -352,34 +410,63 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t stride = nwarps * GPW;
-    const bool staged = FROM_SLOTS && b.pos_info != nullptr;
+    const bool staged = FROM_SLOTS && b.pos_info != nullptr && b.stage;
     auto kof = [&](int64_t ii) -> int64_t {
         return b.klist ? (ii < b.nk ? (int64_t)b.klist[ii] : 0) : ii;
     };
 
     if (staged) {
-        // slot path: records, slots and row offsets of tile n+1 are in flight
-        // while tile n is fitted; klist runs two tiles ahead
+        // cp.async pipeline (StageSmem): records two tiles ahead, support
+        // rows one tile ahead, the fit of the current tile from shared memory
+        using SS = StageSmem<DIM, G, ROWS>;
+        SS &S = *reinterpret_cast<SS *>(smem + block_smem_bytes<G>(0, K) +
+                                        (threadIdx.x / G) * stage_bytes<DIM, G, ROWS>());
         const int64_t ii0 = warp * GPW + lane / G;
-        TileIn<DIM, ROWS> cur;
-        fetch_tile<DIM, G, ROWS, SOLVE>(b, ii0, kof(ii0), glane, cur);
-        int64_t k_next = kof(ii0 + stride);
-        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
+        stage_records<DIM, G, ROWS, SOLVE>(b, S, 0, ii0 < b.nk, kof(ii0), glane);
+        cp_async_commit();
+        stage_records<DIM, G, ROWS, SOLVE>(b, S, 1, ii0 + stride < b.nk, kof(ii0 + stride),
+                                           glane);
+        cp_async_commit();
+        int64_t k_next = kof(ii0 + 2 * stride);
+        cp_async_wait_all();
+        __syncwarp();
+        stage_rows<DIM, G, ROWS>(s, b, S, 0, 0, glane);
+        cp_async_commit();
+        int n = 0;
+        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps, n++) {
             const int64_t ii = tile * GPW + lane / G;
-            TileIn<DIM, ROWS> nxt;
-            fetch_tile<DIM, G, ROWS, SOLVE>(b, ii + stride, k_next, glane, nxt);
-            k_next = kof(ii + 2 * stride);
+            const int cs = n % 3, cb = n & 1;
+            cp_async_wait_all();  // rows of tile n, records of tile n+1
+            __syncwarp();
+            stage_rows<DIM, G, ROWS>(s, b, S, (n + 1) % 3, cb ^ 1, glane);
+            cp_async_commit();
+            stage_records<DIM, G, ROWS, SOLVE>(b, S, (n + 2) % 3, ii + 2 * stride < b.nk, k_next,
+                                               glane);
+            cp_async_commit();
+            k_next = kof(ii + 3 * stride);
+            const auto &R = S.rec[cs];
+            const PosInfo pi = R.pi;
+            int m = pi.m;
             bool active = ii < b.nk;
-            int m = cur.pi.m;
             if (m > b.slot_cap) {  // overflow: built by the rescan launch
                 active = false;
                 m = 0;
             }
-            build_one<DIM, DEG, G, ROWS, SOLVE>(s, b, gs, lane, glane, active, cur.k, cur.pi.tid,
-                                                cur.t, cur.pi.r, m, cur.spos, cur.off, nfail,
-                                                first_fail);
-            cur = nxt;
+            double t[DIM], p[ROWS][DIM];
+            int32_t ids[ROWS];
+#pragma unroll
+            for (int a = 0; a < DIM; a++) t[a] = R.t[a];
+#pragma unroll
+            for (int q = 0; q < ROWS; q++) {
+                const int i = q * G + glane;
+#pragma unroll
+                for (int a = 0; a < DIM; a++) p[q][a] = S.pts[cb][i][a];
+                ids[q] = S.ids[cb][i];
+            }
+            build_core<DIM, DEG, G, ROWS, SOLVE>(b, gs, lane, glane, active, pi.tid, t, pi.r, m,
+                                                 p, ids, SOLVE ? 0 : R.off, nfail, first_fail);
         }
+        cp_async_wait_all();
     } else {
         for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
             const int64_t ii = tile * GPW + lane / G;
@@ -759,6 +846,15 @@ int launch_fill(const SearchArgs &s, const int64_t *offsets, int cap, int64_t *i
     return FM_OK;
 }
 
+// FM_BUILD_STAGE=0 disables the cp.async build pipeline (A/B checks)
+inline bool build_stage_enabled() {
+    static const int v = [] {
+        const char *e = getenv("FM_BUILD_STAGE");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v != 0;
+}
+
 // Largest fit (rows) built with 4-lane groups; FM_BUILD_G4=<rows> overrides
 // (0 disables them; A/B checks)
 inline int build_g4_rows() {
@@ -827,10 +923,14 @@ inline int fit_rows_needed(int max_m, int K, double lam) {
 }
 
 template <int DIM, int DEG, int G, int ROWS, bool SOLVE, bool FROM_SLOTS>
-int launch_build_rows(const SearchArgs &s, const BuildArgs &b, cudaStream_t st) {
+int launch_build_rows(const SearchArgs &s, const BuildArgs &b0, cudaStream_t st) {
     constexpr int K = Monos<DIM, DEG>::K;
-    const size_t sm = block_smem_bytes<G>(FROM_SLOTS ? 0 : b.cap, K);
+    BuildArgs b = b0;
+    size_t sm = block_smem_bytes<G>(FROM_SLOTS ? 0 : b.cap, K);
     if (sm > 200 * 1024) return FM_ERR_UNSUPPORTED;
+    const size_t staged = sm + (size_t)(kBlock / G) * stage_bytes<DIM, G, ROWS>();
+    b.stage = FROM_SLOTS && b.pos_info && staged <= 75 * 1024 && build_stage_enabled();
+    if (b.stage) sm = staged;
     auto kern = k_build<DIM, DEG, G, ROWS, SOLVE, FROM_SLOTS>;
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
