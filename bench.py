@@ -202,12 +202,13 @@ def fit_flops(counts, k):
 # ------------------------------------------------------------ b200 arm
 # kernels launched by one device step (our own, counted from the launch
 # sequence in device.py / libfieldmap.so and checked against the ncu launch
-# list): source bbox 3, grid build 7, target order 5, target bbox 3, select 2,
-# ordered offsets + size buckets 4, operator build 1 + one per non-empty size
-# bucket (+1 if some support overflows its slot), apply 1
+# list, profiles/): bbox pair 1; grid build: cell keys, scan, scatter,
+# in-cell sort 4; target order: keys, scan, scatter 3; select: stats init +
+# select 2; ordered offsets: gather counts + scan 2; build: stats init + one
+# per non-empty size bucket (+1 if some support overflows its slot); apply 1
 def launches_per_step(sel):
     buckets = int(np.count_nonzero(sel.bucket_count)) if sel.bucket_count is not None else 1
-    return 3 + 7 + 5 + 3 + 2 + 4 + 1 + buckets + (1 if sel.n_overflow else 0) + 1
+    return 1 + 4 + 3 + 2 + 2 + 1 + buckets + (1 if sel.n_overflow else 0) + 1
 
 
 def b200_step(src_d, tgt_d, X_d, spec, marks):
