@@ -248,7 +248,7 @@ def run_b200(args, rank, world, local_rank):
 
     from paper_2510_18838_b200 import device as D
     from paper_2510_18838_b200 import pointwise as P
-    from paper_2510_18838_b200.distributed import gather_target_field
+    from paper_2510_18838_b200.distributed import map_gathered
 
     torch.cuda.set_device(local_rank)
     src, tgt, X, spec, desc = workload(args.config, rank)
@@ -257,14 +257,13 @@ def run_b200(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def step(marks):
-        Y, op, cnt, stats, cloud = b200_step(src_d, tgt_d, X_d, spec, marks)
-        Yl = Y
         if world > 1:
-            Y = gather_target_field(Y, nt_local * world)
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            marks.append(("allgather", e))
-        return Y, op, cnt, stats, (cloud, Yl)
+            # blocks of this rank's targets, each block's rows all-gathered on
+            # a side stream behind the next block's build (distributed.py)
+            Y = map_gathered(src_d, tgt_d, X_d, spec, nblocks=args.blocks, marks=marks)
+            return Y, None, None, torch.zeros(1, dtype=torch.int32), (None, Y)
+        Y, op, cnt, stats, cloud = b200_step(src_d, tgt_d, X_d, spec, marks)
+        return Y, op, cnt, stats, (cloud, Y)
 
     sampler = ClockSampler(local_rank)
     with sampler:
@@ -298,12 +297,21 @@ def run_b200(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     value = nt_local * world * args.steps / (total_ms * 1e-3)
 
+    if world > 1:
+        # roofline inputs from one single-block pass on this rank (after the
+        # timed region; the pipelined step interleaves builds and gathers)
+        m1 = []
+        Y1, op, cnt, stats, _c = b200_step(src_d, tgt_d, X_d, spec, m1)
+        torch.cuda.synchronize()
+        ph1 = {b: ea.elapsed_time(eb) for (a, ea), (b, eb) in zip(m1[:-1], m1[1:])}
+        build_ms, apply_ms = ph1["build"], ph1["apply"]
+    else:
+        build_ms = phase["build"] / args.steps
+        apply_ms = phase["apply"] / args.steps
     # roofline inputs (per launch, from this run's own CUDA events)
     counts = cnt.counts.cpu().numpy()
     k = P.n_monomials(spec.degree, 2)
     flops = fit_flops(counts, k)
-    build_ms = phase["build"] / args.steps
-    apply_ms = phase["apply"] / args.steps
     C = X.shape[1]
     apply_bytes = op.algorithmic_bytes(C)
     peaks = measured_peaks()
@@ -324,12 +332,14 @@ def run_b200(args, rank, world, local_rank):
                 # reads back its own rows (the field is complete across the
                 # ranks' hosts -- copying all of it to every host would cost
                 # N x the PCIe traffic for the same data)
-                Yd = P.fit_point_cloud(src_h, X_h.to("cuda", non_blocking=True), tgt_h, spec)
-                Yf = gather_target_field(Yd, nt_local * world)
-                Yh = torch.empty(Yd.shape, dtype=Yd.dtype, pin_memory=True)
-                Yh.copy_(Yd, non_blocking=True)
+                sd = src_h.to("cuda", non_blocking=True)
+                td = tgt_h.to("cuda", non_blocking=True)
+                Xd = X_h.to("cuda", non_blocking=True)
+                Yf = map_gathered(sd, td, Xd, spec, nblocks=args.blocks)
+                r0 = rank * nt_local
+                Yh = torch.empty((nt_local, Yf.shape[1]), dtype=Yf.dtype, pin_memory=True)
+                Yh.copy_(Yf[r0:r0 + nt_local], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
-                del Yf
                 return Yh.numpy()
             # one-shot transfer of the 8-component field (pointwise.py:434):
             # host pinned buffers in, pinned host result out
@@ -640,6 +650,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--blocks", type=int, default=4,
+                    help="N>1: target blocks per rank (all-gather pipelining depth)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))

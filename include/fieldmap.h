@@ -143,6 +143,13 @@ int fm_grid_geometry(int dim, const double *bbox_lo, const double *bbox_hi, int6
  * blocks of 8x8 (2-D), 4x4x4 (3-D) or 2^dim cells, block-major.  Results
  * never depend on it; perm[k] = target processed k-th. */
 size_t fm_order_workspace(int64_t nt, const fm_grid *grid);
+/* Same with the targets in nblocks index blocks [nt*b/nblocks,
+ * nt*(b+1)/nblocks), block-major: the processing positions of block b are
+ * exactly that index range (each block in cell-block order). */
+size_t fm_order_workspace_blocked(int64_t nt, const fm_grid *grid, int32_t nblocks);
+int fm_target_order_blocked(const fm_grid *grid, const double *targets, int64_t nt,
+                            int32_t nblocks, int32_t *perm, void *workspace,
+                            size_t workspace_bytes, fm_stream_t stream);
 int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
                     void *workspace, size_t workspace_bytes, fm_stream_t stream);
 
@@ -241,6 +248,16 @@ int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, in
                        int64_t *offsets, int32_t *bucket_list, int32_t *bucket_count,
                        void *workspace, size_t workspace_bytes, fm_stream_t stream);
 
+/* Bucket lists (as fm_offsets_ordered's) of the processing positions
+ * [p0, p1) only: positions (absolute) by support size into
+ * bucket_list[b * bucket_stride + i], sizes into the DEVICE array
+ * bucket_count[FM_NBUCKETS].  With fm_target_order_blocked the positions of
+ * a target block are such a range, so the operator rows of one block can be
+ * built (fm_lists.bucket_count_dev) while another block's results move. */
+int fm_bucket_positions(const int32_t *counts, const int32_t *perm, int64_t p0, int64_t p1,
+                        int32_t slot_cap, int32_t *bucket_list, int64_t bucket_stride,
+                        int32_t *bucket_count, fm_stream_t stream);
+
 /* Supports produced by fm_select (device pointers; n_overflow is the host
  * copy of stats[6]).  With bucket_list (fm_offsets_ordered's, stride
  * bucket_stride = nt, bucket_count = host copy of its counts) the build
@@ -254,9 +271,15 @@ typedef struct fm_lists {
     const int32_t *overflow;
     const void *pos_info;       /* optional, from fm_select_supports */
     const double *pos_targets;  /* optional, from fm_select_supports */
-    const int32_t *bucket_list; /* optional, from fm_offsets_ordered */
+    const int32_t *bucket_list; /* optional, from fm_offsets_ordered / fm_bucket_positions */
     int64_t bucket_stride;
     int32_t bucket_count[FM_NBUCKETS];
+    /* optional device-side bucket sizes (fm_bucket_positions): when set, the
+     * buckets whose bit is set in bucket_mask are launched with their sizes
+     * read on the device (bucket_count is ignored; no host sync needed) */
+    const int32_t *bucket_count_dev;
+    int32_t bucket_mask;
+    int32_t skip_overflow; /* nonzero: do not rebuild the overflow positions in this call */
 } fm_lists;
 
 /* --------------------------------- a8/a13: transfer operator (new)

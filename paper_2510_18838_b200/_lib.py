@@ -52,7 +52,8 @@ class FmLists(ctypes.Structure):
     _fields_ = [("counts", c_vp), ("slot_id", c_vp), ("slot_pos", c_vp), ("slot_cap", c_i32),
                 ("n_overflow", c_i32), ("overflow", c_vp), ("pos_info", c_vp),
                 ("pos_targets", c_vp), ("bucket_list", c_vp), ("bucket_stride", c_i64),
-                ("bucket_count", c_i32 * FM_NBUCKETS)]
+                ("bucket_count", c_i32 * FM_NBUCKETS), ("bucket_count_dev", c_vp),
+                ("bucket_mask", c_i32), ("skip_overflow", c_i32)]
 
 
 P = ctypes.POINTER
@@ -68,6 +69,9 @@ SIGNATURES = {
     "fm_grid_geometry": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_dbl, P(FmGrid), c_vp, c_vp]),
     "fm_order_workspace": (c_sz, [c_i64, P(FmGrid)]),
     "fm_target_order": (c_i32, [P(FmGrid), c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "fm_order_workspace_blocked": (c_sz, [c_i64, P(FmGrid), c_i32]),
+    "fm_target_order_blocked": (c_i32, [P(FmGrid), c_vp, c_i64, c_i32, c_vp, c_vp, c_sz, c_vp]),
+    "fm_bucket_positions": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp]),
     "fm_support_count": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect), c_i32,
                                  c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fm_scan_workspace": (c_sz, [c_i64]),
@@ -91,6 +95,17 @@ SIGNATURES = {
                                    c_vp, c_vp]),
     "fm_apply": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
     "fm_fp64_probe": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp]),
+    # include/fieldmap_dist.h
+    "fm_ipc_handle_size": (c_i32, []),
+    "fm_device_alloc": (c_i32, [c_sz, P(c_vp)]),
+    "fm_device_free": (c_i32, [c_vp]),
+    "fm_ipc_export": (c_i32, [c_vp, c_vp]),
+    "fm_ipc_open": (c_i32, [c_vp, P(c_vp)]),
+    "fm_ipc_close": (c_i32, [c_vp]),
+    "fm_build_apply_blocks": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
+                                      c_vp, P(FmLists), c_vp, c_i32, P(FmRbf), P(FmFit), c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp,
+                                      c_i32, c_vp, c_vp, c_vp]),
     # include/fieldmap_patch.h
     "fm_patch_count": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp,
                                c_vp]),

@@ -1,6 +1,7 @@
 // fm_api.cu -- extern "C" entry points (include/fieldmap.h), the radial
 // weight kernel, the operator apply (SpMM) kernel and the FP64 probe.
 #include <algorithm>
+#include <cstdlib>
 
 #include "fm_kernels.cuh"
 #include "fm_scan.cuh"
@@ -309,6 +310,36 @@ static int dispatch_build(int dim, int degree, bool solve, bool slots, const Sea
     return FM_ERR_UNSUPPORTED;
 }
 
+// Size-bucket launches of one build run concurrently on side streams
+// (fork/join with events on the caller's stream): the buckets' kernels
+// overlap each other's tails.  FM_BUILD_CONCURRENT=0 serialises them.
+struct BucketStreams {
+    cudaStream_t s[FM_NBUCKETS];
+    cudaEvent_t fork, join[FM_NBUCKETS];
+    bool ok = false;
+};
+
+static BucketStreams *bucket_streams() {
+    static BucketStreams pool[64];
+    static const bool enabled = [] {
+        const char *e = getenv("FM_BUILD_CONCURRENT");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    BucketStreams &b = pool[dev];
+    if (!b.ok) {
+        bool good = cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < FM_NBUCKETS && good; i++)
+            good = cudaStreamCreateWithFlags(&b.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+                   cudaEventCreateWithFlags(&b.join[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!good) return nullptr;
+        b.ok = true;
+    }
+    return &b;
+}
+
 static int build_common(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
                         const int32_t *sorted_ids, const double *targets, int64_t nt,
                         const int32_t *perm, const fm_select *sel, const double *radii,
@@ -322,7 +353,8 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
     if (sel->adaptive && !radii) return FM_ERR_ARG;
     if (lists && (!lists->counts || !lists->slot_pos || lists->slot_cap < 1 ||
                   lists->n_overflow < 0 || (lists->n_overflow > 0 && !lists->overflow) ||
-                  (lists->bucket_list && lists->bucket_stride < nt)))
+                  (lists->bucket_list && !lists->bucket_count_dev &&
+                   lists->bucket_stride < nt)))
         return FM_ERR_ARG;
     const SearchArgs s = make_search(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm,
                                      sel, sel->adaptive ? radii : nullptr);
@@ -351,22 +383,43 @@ static int build_common(const fm_grid *grid, const int32_t *cell_start, const do
         const int mm = max_count < lists->slot_cap ? max_count : lists->slot_cap;
         if (lists->bucket_list) {
             // one launch per non-empty size bucket, each with the fit shape
-            // (lanes x rows per lane) of the bucket's largest support
+            // (lanes x rows per lane) of the bucket's largest support.  With
+            // bucket_count_dev the sizes are read on the device (no host
+            // sync): the buckets of bucket_mask run over at most bucket_stride
+            // positions each.
             constexpr int edges[FM_NBUCKETS] = FM_BUCKET_EDGES;
-            for (int bk = 0; bk < FM_NBUCKETS; bk++) {
-                if (lists->bucket_count[bk] <= 0) continue;
+            const bool dev_counts = lists->bucket_count_dev != nullptr;
+            int used[FM_NBUCKETS], nused = 0;
+            for (int bk = 0; bk < FM_NBUCKETS; bk++)
+                if (dev_counts ? (lists->bucket_mask & (1 << bk)) != 0
+                               : lists->bucket_count[bk] > 0)
+                    used[nused++] = bk;
+            BucketStreams *bs = nused > 1 ? bucket_streams() : nullptr;
+            if (bs) cudaEventRecord(bs->fork, st);
+            for (int u = 0; u < nused; u++) {
+                const int bk = used[u];
                 BuildArgs bb = b;
                 bb.klist = lists->bucket_list + (int64_t)bk * lists->bucket_stride;
-                bb.nk = lists->bucket_count[bk];
+                bb.nk = dev_counts ? lists->bucket_stride : lists->bucket_count[bk];
+                bb.nk_dev = dev_counts ? lists->bucket_count_dev + bk : nullptr;
+                cudaStream_t sb = st;
+                if (bs) {
+                    sb = bs->s[u];
+                    cudaStreamWaitEvent(sb, bs->fork, 0);
+                }
                 rc = dispatch_build(grid->dim, fit->degree, solve, true, s, bb,
-                                    edges[bk] < mm ? edges[bk] : mm, st);
+                                    edges[bk] < mm ? edges[bk] : mm, sb);
+                if (bs) {
+                    cudaEventRecord(bs->join[u], sb);
+                    cudaStreamWaitEvent(st, bs->join[u], 0);
+                }
                 if (rc) return rc;
             }
         } else {
             rc = dispatch_build(grid->dim, fit->degree, solve, true, s, b, mm, st);
             if (rc) return rc;
         }
-        if (lists->n_overflow == 0) return FM_OK;
+        if (lists->n_overflow == 0 || lists->skip_overflow) return FM_OK;
         b.klist = lists->overflow;
         b.nk = lists->n_overflow;
     }
@@ -444,6 +497,25 @@ int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, in
         FM_CHECK_LAUNCH();
     }
     return exclusive_scan<int32_t, int64_t>(tmp, n, offsets, scan_ws, scan_workspace_bytes(n), st);
+}
+
+int fm_bucket_positions(const int32_t *counts, const int32_t *perm, int64_t p0, int64_t p1,
+                        int32_t slot_cap, int32_t *bucket_list, int64_t bucket_stride,
+                        int32_t *bucket_count, fm_stream_t stream) {
+    if (p0 < 0 || p1 < p0 || !counts || !bucket_list || !bucket_count ||
+        bucket_stride < p1 - p0)
+        return FM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(bucket_count, 0, sizeof(int32_t) * FM_NBUCKETS, st) != cudaSuccess)
+        return FM_ERR_CUDA;
+    const int64_t n = p1 - p0;
+    if (n > 0) {
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
+        k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, nullptr, slot_cap, bucket_list,
+                                                bucket_count, p0, bucket_stride);
+        FM_CHECK_LAUNCH();
+    }
+    return FM_OK;
 }
 
 int fm_apply(int64_t nt, const int64_t *row_off, const int32_t *col, const double *val,

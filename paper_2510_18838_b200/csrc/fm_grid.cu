@@ -59,15 +59,26 @@ static int64_t order_keys(const fm_grid *grid) {
     return nk;
 }
 
+// nblocks > 1: targets in index blocks [n*b/nblocks, n*(b+1)/nblocks) come
+// block by block (block-major keys), each block in cell-block order -- the
+// positions of target block b are then the contiguous range of processing
+// positions [n*b/nblocks, n*(b+1)/nblocks).
 template <int DIM>
 __global__ void k_order_keys(GridDev g, const double *__restrict__ pts, int64_t n,
-                             int32_t *__restrict__ keys, int32_t *__restrict__ counts) {
+                             int32_t *__restrict__ keys, int32_t *__restrict__ counts,
+                             int nblocks, int64_t nkeys) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double p[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; a++) p[a] = pts[i * DIM + a];
-        const int32_t c = (int32_t)order_key<DIM>(g, p);
+        int64_t blk = 0;
+        if (nblocks > 1) {  // largest b with n*b/nblocks <= i
+            blk = (i * nblocks) / n;
+            while (blk + 1 < nblocks && n * (blk + 1) / nblocks <= i) blk++;
+            while (blk > 0 && n * blk / nblocks > i) blk--;
+        }
+        const int32_t c = (int32_t)(blk * nkeys + order_key<DIM>(g, p));
         keys[i] = c;
         atomicAdd(&counts[c], 1);
     }
@@ -272,11 +283,13 @@ __global__ void k_bbox_final(const unsigned long long *acc, int dim, double *loh
 
 template <int DIM>
 static int launch_keys(const GridDev &g, const double *pts, int64_t n, int32_t *keys,
-                       int32_t *counts, cudaStream_t s, bool order = false) {
+                       int32_t *counts, cudaStream_t s, bool order = false, int nblocks = 1,
+                       int64_t nkeys = 0) {
     const int threads = 256;
     const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
     if (blocks && order)
-        k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
+        k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts, nblocks,
+                                                                 nkeys);
     else if (blocks)
         k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
     FM_CHECK_LAUNCH();
@@ -369,19 +382,26 @@ int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t str
     return FM_OK;
 }
 
-size_t fm_order_workspace(int64_t nt, const fm_grid *grid) {
-    if (!grid || grid->dim < 1 || grid->dim > kMaxDim) return 0;
-    const int64_t nk = order_keys(grid);
+size_t fm_order_workspace_blocked(int64_t nt, const fm_grid *grid, int32_t nblocks) {
+    if (!grid || grid->dim < 1 || grid->dim > kMaxDim || nblocks < 1) return 0;
+    const int64_t nk = order_keys(grid) * nblocks;
     return fm_grid_workspace(nt, nk) + align256(sizeof(int32_t) * (size_t)(nk + 1));
 }
 
-int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
-                    void *workspace, size_t workspace_bytes, fm_stream_t stream) {
-    if (!grid || grid->dim < 1 || grid->dim > kMaxDim || nt < 0 || grid->ncell < 1)
+size_t fm_order_workspace(int64_t nt, const fm_grid *grid) {
+    return fm_order_workspace_blocked(nt, grid, 1);
+}
+
+int fm_target_order_blocked(const fm_grid *grid, const double *targets, int64_t nt,
+                            int32_t nblocks, int32_t *perm, void *workspace,
+                            size_t workspace_bytes, fm_stream_t stream) {
+    if (!grid || grid->dim < 1 || grid->dim > kMaxDim || nt < 0 || grid->ncell < 1 ||
+        nblocks < 1)
         return FM_ERR_ARG;
-    const int64_t ncell = order_keys(grid);  // key range of the blocked order
+    const int64_t nkeys = order_keys(grid);
+    const int64_t ncell = nkeys * nblocks;  // key range of the (block-major) blocked order
     if (nt >= (int64_t)INT32_MAX || ncell >= (int64_t)INT32_MAX) return FM_ERR_UNSUPPORTED;
-    if (workspace_bytes < fm_order_workspace(nt, grid)) return FM_ERR_WORKSPACE;
+    if (workspace_bytes < fm_order_workspace_blocked(nt, grid, nblocks)) return FM_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
     char *w = (char *)workspace;
     int32_t *keys = (int32_t *)w;
@@ -397,11 +417,11 @@ int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int3
     cudaMemsetAsync(counts, 0, (size_t)((char *)(fill + ncell) - (char *)counts), s);
     int rc;
     switch (grid->dim) {
-    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s, true); break;
-    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s, true); break;
-    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s, true); break;
-    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s, true); break;
-    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s, true); break;
+    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
+    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
+    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
+    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
+    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
     }
     if (rc) return rc;
     rc = exclusive_scan<int32_t, int32_t>(counts, ncell, start, scan_ws,
@@ -416,6 +436,10 @@ int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int3
     return FM_OK;
 }
 
+int fm_target_order(const fm_grid *grid, const double *targets, int64_t nt, int32_t *perm,
+                    void *workspace, size_t workspace_bytes, fm_stream_t stream) {
+    return fm_target_order_blocked(grid, targets, nt, 1, perm, workspace, workspace_bytes, stream);
+}
 
 static double host_dval(unsigned long long k) {
     const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;

@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kBlock) k_support_fill(SearchArgs s, const int
 struct BuildArgs {
     const int32_t *klist;  // positions to process, or null for 0..nk-1
     int stage;             // shared memory sized for the cp.async pipeline
-    int64_t nk;
+    int64_t nk;            // positions (upper bound when nk_dev is set)
+    const int32_t *nk_dev;  // optional device-side position count (read at kernel start)
     const int32_t *slot_pos;
     int slot_cap;
     const int32_t *counts;  // support size per target (FROM_SLOTS)
@@ -411,8 +412,9 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t stride = nwarps * GPW;
     const bool staged = FROM_SLOTS && b.pos_info != nullptr && b.stage;
+    const int64_t nk = b.nk_dev ? (int64_t)*b.nk_dev : b.nk;
     auto kof = [&](int64_t ii) -> int64_t {
-        return b.klist ? (ii < b.nk ? (int64_t)b.klist[ii] : 0) : ii;
+        return b.klist ? (ii < nk ? (int64_t)b.klist[ii] : 0) : ii;
     };
 
     if (staged) {
@@ -422,9 +424,9 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
         SS &S = *reinterpret_cast<SS *>(smem + block_smem_bytes<G>(0, K) +
                                         (threadIdx.x / G) * stage_bytes<DIM, G, ROWS>());
         const int64_t ii0 = warp * GPW + lane / G;
-        stage_records<DIM, G, ROWS, SOLVE>(b, S, 0, ii0 < b.nk, kof(ii0), glane);
+        stage_records<DIM, G, ROWS, SOLVE>(b, S, 0, ii0 < nk, kof(ii0), glane);
         cp_async_commit();
-        stage_records<DIM, G, ROWS, SOLVE>(b, S, 1, ii0 + stride < b.nk, kof(ii0 + stride),
+        stage_records<DIM, G, ROWS, SOLVE>(b, S, 1, ii0 + stride < nk, kof(ii0 + stride),
                                            glane);
         cp_async_commit();
         int64_t k_next = kof(ii0 + 2 * stride);
@@ -433,21 +435,21 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
         stage_rows<DIM, G, ROWS>(s, b, S, 0, 0, glane);
         cp_async_commit();
         int n = 0;
-        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps, n++) {
+        for (int64_t tile = warp; tile * GPW < nk; tile += nwarps, n++) {
             const int64_t ii = tile * GPW + lane / G;
             const int cs = n % 3, cb = n & 1;
             cp_async_wait_all();  // rows of tile n, records of tile n+1
             __syncwarp();
             stage_rows<DIM, G, ROWS>(s, b, S, (n + 1) % 3, cb ^ 1, glane);
             cp_async_commit();
-            stage_records<DIM, G, ROWS, SOLVE>(b, S, (n + 2) % 3, ii + 2 * stride < b.nk, k_next,
+            stage_records<DIM, G, ROWS, SOLVE>(b, S, (n + 2) % 3, ii + 2 * stride < nk, k_next,
                                                glane);
             cp_async_commit();
             k_next = kof(ii + 3 * stride);
             const auto &R = S.rec[cs];
             const PosInfo pi = R.pi;
             int m = pi.m;
-            bool active = ii < b.nk;
+            bool active = ii < nk;
             if (m > b.slot_cap) {  // overflow: built by the rescan launch
                 active = false;
                 m = 0;
@@ -468,9 +470,9 @@ __global__ void __launch_bounds__(kBlock, (G == 8 && ROWS <= 2)   ? FM_BUILD_MIN
         }
         cp_async_wait_all();
     } else {
-        for (int64_t tile = warp; tile * GPW < b.nk; tile += nwarps) {
+        for (int64_t tile = warp; tile * GPW < nk; tile += nwarps) {
             const int64_t ii = tile * GPW + lane / G;
-            bool active = ii < b.nk;
+            bool active = ii < nk;
             const int64_t k = active ? kof(ii) : 0;
             const int64_t tid = active ? (s.perm ? (int64_t)s.perm[k] : k) : 0;
             double t[DIM];
@@ -714,27 +716,32 @@ __device__ __forceinline__ int bucket_of(int m) {
 // counts in processing order (input of the ordered offsets scan) and,
 // with bucket_list, the positions partitioned by support size
 // (warp-aggregated appends: one atomic per bucket present in a warp)
+// positions p0 + [0, n): out (may be NULL) indexed from 0, bucket lists
+// with stride lstride holding absolute positions
 static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
                                 const int32_t *__restrict__ perm, int64_t n,
                                 int32_t *__restrict__ out, int slot_cap,
                                 int32_t *__restrict__ bucket_list,
-                                int32_t *__restrict__ bucket_count) {
+                                int32_t *__restrict__ bucket_count, int64_t p0 = 0,
+                                int64_t lstride = -1) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (lstride < 0) lstride = n;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
          base += stride) {
-        const int64_t i = base + lane;
-        const int m = i < n ? counts[perm ? perm[i] : i] : 0;
-        if (i < n) out[i] = m;
+        const int64_t j = base + lane;
+        const int64_t i = p0 + j;
+        const int m = j < n ? counts[perm ? perm[i] : i] : 0;
+        if (j < n && out) out[j] = m;
         if (bucket_list) {
-            const int b = (i < n && m <= slot_cap) ? bucket_of(m) : -1;
+            const int b = (j < n && m <= slot_cap) ? bucket_of(m) : -1;
             const unsigned peers = __match_any_sync(FM_FULL_MASK, b);
             if (b >= 0) {
                 const int leader = __ffs(peers) - 1;
                 int at = 0;
                 if (lane == leader) at = atomicAdd(bucket_count + b, __popc(peers));
                 at = __shfl_sync(peers, at, leader);
-                bucket_list[(int64_t)b * n + at + __popc(peers & ((1u << lane) - 1u))] =
+                bucket_list[(int64_t)b * lstride + at + __popc(peers & ((1u << lane) - 1u))] =
                     (int32_t)i;
             }
         }
@@ -934,7 +941,20 @@ int launch_build_rows(const SearchArgs &s, const BuildArgs &b0, cudaStream_t st)
     auto kern = k_build<DIM, DEG, G, ROWS, SOLVE, FROM_SLOTS>;
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<grid_blocks(b.nk, kBlock / G, 16), kBlock, sm, st>>>(s, b);
+    // persistent grid: the resident CTAs of every SM, grid-striding over
+    // the positions (no waves of CTAs that only run the pipeline prologue,
+    // e.g. when the count is read on the device and nk is an upper bound)
+    static size_t occ_sm = (size_t)-1;
+    static int occ = 1;
+    if (occ_sm != sm) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kBlock, sm) != cudaSuccess ||
+            o < 1)
+            o = 1;
+        occ = o;
+        occ_sm = sm;
+    }
+    kern<<<grid_blocks(b.nk, kBlock / G, occ), kBlock, sm, st>>>(s, b);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }

@@ -99,15 +99,18 @@ class SourceCloud:
                               ptr(ws), ws_bytes, _stream()), "fm_grid_build")
         self._ws = ws  # keep alive until the stream has consumed it
 
-    def target_order(self, targets):
-        """Cell order of `targets` (device int32 perm) for locality."""
+    def target_order(self, targets, nblocks=1):
+        """Cell order of `targets` (device int32 perm) for locality.  With
+        nblocks > 1 the targets of index block b = [nt*b/nblocks,
+        nt*(b+1)/nblocks) occupy exactly those processing positions."""
         L = _lib.lib()
         nt = targets.shape[0]
         perm = _empty(nt, torch.int32, targets.device)
-        ws_bytes = L.fm_order_workspace(nt, ctypes.byref(self.grid))
+        ws_bytes = L.fm_order_workspace_blocked(nt, ctypes.byref(self.grid), int(nblocks))
         ws = _workspace(ws_bytes, targets.device)
-        check(L.fm_target_order(ctypes.byref(self.grid), ptr(targets), nt, ptr(perm), ptr(ws),
-                                ws_bytes, _stream()), "fm_target_order")
+        check(L.fm_target_order_blocked(ctypes.byref(self.grid), ptr(targets), nt, int(nblocks),
+                                        ptr(perm), ptr(ws), ws_bytes, _stream()),
+              "fm_target_order_blocked")
         self._ws_order = ws
         return perm
 

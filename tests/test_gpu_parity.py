@@ -869,3 +869,39 @@ def test_transfer_extrinsic_element_patch(loc):
     assert len(calls) == -(-t.shape[0] // 128)
     assert np.array_equal(got, intr)
     np.testing.assert_allclose(got, d[f"sq_{loc}_fit_2_3"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.gpu
+def test_map_gathered_blocks_equal_one_shot():
+    """distributed.map_gathered (blocks of targets, all-gather pipelined on a
+    side stream) on a one-rank NCCL group: bitwise the one-shot transfer."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_18838_b200 import distributed as Dist
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200 import synth
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        m = synth.disk_graded(1.0, 60, 0.6)
+        src = m.coords
+        tgt = synth.disk(1.0, 50).coords
+        X = synth.sincos_field(src, 8)
+        h = m.mean_edge_length
+        spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.AdaptiveRadius(12, h, 1.5))
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        want = P.fit_point_cloud(d(src), d(X), d(tgt), spec)
+        for nb in (1, 3, 7):
+            got = Dist.map_gathered(d(src), d(tgt), d(X), spec, nblocks=nb)
+            assert torch.equal(got, want), nb
+    finally:
+        dist.destroy_process_group()
