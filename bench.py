@@ -256,11 +256,20 @@ def run_b200(args, rank, world, local_rank):
     src_d, tgt_d, X_d = D.to_device(src), D.to_device(tgt), D.to_device(X)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
+    pending = []
+
     def step(marks):
         if world > 1:
-            # blocks of this rank's targets, each block's rows all-gathered on
-            # a side stream behind the next block's build (distributed.py)
-            Y = map_gathered(src_d, tgt_d, X_d, spec, nblocks=args.blocks, marks=marks)
+            # blocks of this rank's targets; each block's rows pushed to the
+            # peers (copy engines, NVLink) behind the next block's build, and
+            # the exchange of this step completing under the next step
+            # (distributed.map_gathered pipelined); the timed region ends
+            # after the last exchange has completed
+            Y, done = map_gathered(src_d, tgt_d, X_d, spec, nblocks=args.blocks, marks=marks,
+                                   pipelined=True)
+            pending.append(done)
+            while len(pending) > 1:
+                pending.pop(0)
             return Y, None, None, torch.zeros(1, dtype=torch.int32), (None, Y)
         Y, op, cnt, stats, cloud = b200_step(src_d, tgt_d, X_d, spec, marks)
         return Y, op, cnt, stats, (cloud, Y)
@@ -279,7 +288,31 @@ def run_b200(args, rank, world, local_rank):
         phase = {}
         step_ms = []
         sampler.mark_timed()
-        for _ in range(args.steps):
+        if world > 1:
+            for d in pending:
+                d.wait()
+            pending.clear()
+            torch.cuda.synchronize()
+            dist.barrier()
+            torch.cuda.synchronize()
+            # pipelined steps: one event pair around the whole loop (L2
+            # flushes included -- conservative), ended after the last exchange
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                flush.zero_()
+                marks = []
+                Y, op, cnt, stats, extra = step(marks)
+                for (a, ea), (b, eb) in zip(marks[:-1], marks[1:]):
+                    phase.setdefault(b, []).append((ea, eb))
+            for d in pending:
+                d.wait()
+            e1.record()
+            torch.cuda.synchronize()
+            phase = {b: sum(ea.elapsed_time(eb) for ea, eb in v) for b, v in phase.items()}
+            step_ms = [e0.elapsed_time(e1)]
+        for _ in range(args.steps if world == 1 else 0):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             marks = []
             Y, op, cnt, stats, extra = step(marks)
@@ -650,7 +683,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
-    ap.add_argument("--blocks", type=int, default=4,
+    ap.add_argument("--blocks", type=int, default=1,
                     help="N>1: target blocks per rank (all-gather pipelining depth)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

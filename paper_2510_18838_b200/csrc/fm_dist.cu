@@ -20,6 +20,30 @@
 #include "../../include/fieldmap.h"
 #include "../../include/fieldmap_dist.h"
 
+namespace {
+// one stream per peer: the pushes of a block to different peers run on
+// different copy engines concurrently (one stream would serialise them)
+struct PeerStreams {
+    cudaStream_t s[FM_MAX_PEERS];
+    cudaEvent_t join[FM_MAX_PEERS];
+    int n = 0;
+};
+
+PeerStreams *peer_streams(int npeers) {
+    static PeerStreams pool[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    PeerStreams &p = pool[dev];
+    while (p.n < npeers) {
+        if (cudaStreamCreateWithFlags(&p.s[p.n], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p.join[p.n], cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+        p.n++;
+    }
+    return &p;
+}
+}  // namespace
+
 extern "C" {
 
 int fm_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
@@ -103,14 +127,20 @@ int fm_build_apply_blocks(const fm_grid *grid, const int32_t *cell_start,
             }
             evs.push_back(ev);
             cudaEventRecord(ev, st);
-            cudaStreamWaitEvent(cs, ev, 0);
+            PeerStreams *ps = peer_streams(npeers);
             const size_t bytes = (size_t)(hi - lo) * ncomp * sizeof(double);
             for (int q = 0; q < npeers; q++) {
+                cudaStream_t sq = ps ? ps->s[q] : cs;
+                cudaStreamWaitEvent(sq, ev, 0);
                 double *dst = reinterpret_cast<double *>(peer_Y[q]) + lo * ncomp;
-                if (cudaMemcpyAsync(dst, Y + lo * ncomp, bytes, cudaMemcpyDeviceToDevice, cs) !=
+                if (cudaMemcpyAsync(dst, Y + lo * ncomp, bytes, cudaMemcpyDeviceToDevice, sq) !=
                     cudaSuccess) {
                     rc = FM_ERR_CUDA;
                     break;
+                }
+                if (ps) {
+                    cudaEventRecord(ps->join[q], sq);
+                    cudaStreamWaitEvent(cs, ps->join[q], 0);
                 }
             }
         }

@@ -109,15 +109,19 @@ class _Exchange:
 _EXCHANGES = {}
 
 
-def _exchange(world, rank, nt, C, group):
-    key = (torch.cuda.current_device(), world, rank, nt, C, id(group))
+def _exchange(world, rank, nt, C, group, slot=0):
+    key = (torch.cuda.current_device(), world, rank, nt, C, id(group), slot)
     ex = _EXCHANGES.get(key)
     if ex is None:
         ex = _EXCHANGES[key] = _Exchange(world, rank, nt, C, group)
     return ex
 
 
-def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None):
+_PARITY = {}
+
+
+def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None,
+                 pipelined=False):
     """Target-sharded transfer of this rank's targets with the full target
     field delivered to every rank WHILE the operator is built: one grid, one
     target order whose processing positions come block by block
@@ -133,7 +137,13 @@ def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None):
     the next call with the same shapes overwrites.
 
     Selection / fit failures raise the reference's exceptions naming the
-    rank-local target.  `marks` (list) receives (name, cuda event) pairs."""
+    rank-local target.  `marks` (list) receives (name, cuda event) pairs.
+
+    pipelined=True returns (field, done) without waiting for the exchange:
+    the peers' rows keep arriving (copy engines) while the caller goes on --
+    e.g. maps the next batch; `done.wait()` (a torch.distributed Work) makes
+    the current stream wait until the field is complete.  Two receive buffers
+    alternate, so a field stays valid until the call after next."""
     from . import device as D
     from . import pointwise as P
     from ._lib import FmRbf, ptr
@@ -176,7 +186,12 @@ def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None):
             f"target {i} of rank {rank}: only {int(sl.counts[i].item())} sources in the whole "
             f"domain, min_points is {sel.min_points}")
     mark("select")
-    ex = _exchange(world, rank, nt, C, group)
+    slot = 0
+    if pipelined:
+        pk = (torch.cuda.current_device(), world, nt, C, id(group))
+        slot = _PARITY.get(pk, 0)
+        _PARITY[pk] = slot ^ 1
+    ex = _exchange(world, rank, nt, C, group, slot)
     Y = ex.full[rank]
     dev = tgt_d.device
     nnz = sl.nnz
@@ -202,13 +217,15 @@ def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None):
         ctypes.c_void_p(main.cuda_stream), ctypes.c_void_p(comm.cuda_stream)),
         "fm_build_apply_blocks")
     mark("blocks")
+    work = None
     if world > 1:
         # every rank's pushes precede its contribution to this collective on
         # its side stream: once it completes here, all peers' rows have landed
         with torch.cuda.stream(comm):
-            done = torch.zeros(1, dtype=torch.float32, device=dev)
-            dist.all_reduce(done, group=group)
-        main.wait_stream(comm)
+            flag = torch.zeros(1, dtype=torch.float32, device=dev)
+            work = dist.all_reduce(flag, group=group, async_op=pipelined)
+        if not pipelined:
+            main.wait_stream(comm)
     mark("exchange")
     st = stats.view(nblocks, 2)
     if int(st[:, 0].sum().item()) > 0:
@@ -216,7 +233,15 @@ def map_gathered(src_d, tgt_d, X_d, fitspec, nblocks=4, group=None, marks=None):
         raise P.SingularFitError(f"target {bad} of rank {rank}: fit failed "
                                  f"(status {int(status[bad].item())})")
     out = ex.full.reshape(world * nt, C)
-    return out[:, 0] if X_d.ndim == 1 else out
+    out = out[:, 0] if X_d.ndim == 1 else out
+    if pipelined:
+        return out, (work if work is not None else _Done())
+    return out
+
+
+class _Done:
+    def wait(self):
+        return True
 
 
 def _lib():
