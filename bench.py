@@ -462,6 +462,216 @@ def run_b200(args, rank, world, local_rank):
     return line
 
 
+# --------------------------------------------------- C3 / C4 / C5 configs
+LARGE = ("c3", "c3mq", "c4", "c5")
+
+
+def workload_large(config, rank, world, scale=1.0):
+    """BASELINE.json configs[2..4].  `scale` shrinks
+    the point counts (tests / quick checks); 1.0 is the configuration."""
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200.distributed import shard_bounds
+
+    if config in ("c3", "c3mq"):
+        # 16M random sources -> 16M random targets, Gaussian / multiquadric,
+        # AdaptiveRadius(12, 1.5/sqrt(N), 1.5), degree 2, scalar; the 16M
+        # targets split across the ranks (strong scaling)
+        n = int(16_000_000 * scale)
+        src = np.random.RandomState(1).uniform(0, 1, (n, 2))
+        lo, hi = shard_bounds(n, rank, world)
+        tgt = np.ascontiguousarray(np.random.RandomState(2).uniform(0, 1, (n, 2))[lo:hi])
+        X = np.sin(src[:, :1]) * np.cos(src[:, 1:]) + 2.0
+        kind = P.RbfKind.GAUSSIAN if config == "c3" else P.RbfKind.MULTIQUADRIC
+        spec = P.FitSpec(2, P.RadialBasisSpec(kind, a=2.0),
+                         P.AdaptiveRadius(12, 1.5 / math.sqrt(n), 1.5))
+        desc = {"workload": f"C3: {n} random sources -> {n} random targets (RandomState 1/2), "
+                            f"{kind.name.lower()} a=2, AdaptiveRadius(12, 1.5/sqrt(N), 1.5), "
+                            "degree 2, scalar, targets split across ranks",
+                "sources": n, "targets_total": n, "components": 1, "degree": 2}
+        return src, tgt, X, spec, desc, dict(scaling="strong", total=n, metric=None,
+                                             applies=1, chunk=n, gather=False)
+    if config == "c4":
+        # 5-D distribution function: GNET-like tensor source grid 64^2 (space)
+        # x 16^3 (velocity) on [0,1]^5 -> 64M random GTC-like targets, degree 1,
+        # per-axis metric making the source lattice isotropic, operator built
+        # once per step and applied to 32 successive fields
+        ns_ax = [max(2, int(round(v * scale ** 0.2))) for v in (64, 64, 16, 16, 16)]
+        axes = [np.linspace(0.0, 1.0, k) for k in ns_ax]
+        g = np.meshgrid(*axes, indexing="ij")
+        src = np.ascontiguousarray(np.stack([a.reshape(-1) for a in g], axis=1))
+        n = int(64_000_000 * scale)
+        lo, hi = shard_bounds(n, rank, world)
+        rs = np.random.RandomState(4)
+        tgt = np.ascontiguousarray(rs.uniform(0, 1, (n, 5))[lo:hi]) if scale < 1 else None
+        if tgt is None:  # 64M x 5 at full scale: only this rank's rows
+            tgt = np.empty((hi - lo, 5))
+            done = 0
+            while done < n:  # the same stream as uniform(0, 1, (n, 5)), row blocks
+                k = min(4_000_000, n - done)
+                blk = rs.uniform(0, 1, (k, 5))
+                a, b = max(lo, done), min(hi, done + k)
+                if a < b:
+                    tgt[a - lo:b - lo] = blk[a - done:b - done]
+                done += k
+        v = src[:, 2:]
+        X = (np.exp(-np.sum((v - 0.5) ** 2, axis=1) * 8.0) *
+             (1.0 + 0.1 * np.sin(6.0 * src[:, 0]) * np.cos(6.0 * src[:, 1])))[:, None]
+        hs = 1.0 / (ns_ax[0] - 1)
+        metric = [1.0, 1.0] + [(ns_ax[2] - 1) * hs] * 3  # velocity spacing -> spatial spacing
+        spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
+                         P.AdaptiveRadius(12, hs, 1.5))
+        desc = {"workload": f"C4: 5-D tensor source grid {'x'.join(map(str, ns_ax))} on [0,1]^5 "
+                            f"-> {n} random targets (RandomState 4), per-axis metric "
+                            f"{metric}, degree 1, C4 a=2, AdaptiveRadius(12, h, 1.5), operator "
+                            "built once per step then applied to 32 fields",
+                "sources": int(src.shape[0]), "targets_total": n, "components": 1,
+                "degree": 1, "applies": 32}
+        return src, tgt, X, spec, desc, dict(scaling="strong", total=n, metric=metric,
+                                             applies=32, chunk=16_000_000, gather=False)
+    if config == "c5":
+        # 3-D degree 3, 128M targets per GPU (RandomState(5 + rank)) against a
+        # replicated 16M random source cloud, all-gather of the full field
+        ns = int(16_000_000 * scale)
+        nt = int(128_000_000 * scale)
+        src = np.random.RandomState(1).uniform(0, 1, (ns, 3))
+        tgt = np.random.RandomState(5 + rank).uniform(0, 1, (nt, 3))
+        X = (np.sin(3 * src[:, 0]) * np.cos(2 * src[:, 1]) * np.exp(src[:, 2]))[:, None] + 2.0
+        h = ns ** (-1.0 / 3.0)
+        spec = P.FitSpec(3, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.AdaptiveRadius(40, h, 1.5))
+        desc = {"workload": f"C5: {ns} random 3-D sources (replicated) -> {nt} random targets "
+                            "per GPU (RandomState 5+rank), degree 3 (k=20), C4 a=2, "
+                            "AdaptiveRadius(40, N^-1/3, 1.5), scalar, all-gather of the full "
+                            "target field",
+                "sources": ns, "targets_per_gpu": nt, "components": 1, "degree": 3}
+        return src, tgt, X, spec, desc, dict(scaling="weak", total=nt * world, metric=None,
+                                             applies=1, chunk=16_000_000, gather=True)
+    raise SystemExit(f"unknown config {config}")
+
+
+def run_large(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200.distributed import gather_target_field
+
+    torch.cuda.set_device(local_rank)
+    src, tgt, X, spec, desc, meta = workload_large(args.config, rank, world, args.scale)
+    if meta["metric"] is not None:  # the oracle sees the same IEEE products
+        src = np.ascontiguousarray(src * np.asarray(meta["metric"]))
+        tgt = np.ascontiguousarray(tgt * np.asarray(meta["metric"]))
+    src_d, tgt_d, X_d = D.to_device(src), D.to_device(tgt), D.to_device(X)
+    nt = tgt.shape[0]
+    C = X.shape[1]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    Y = torch.empty((nt, C), dtype=torch.float64, device="cuda")
+    rbf = P._rbf_pair(spec.rbf)
+    sel = spec.selection
+    need = 0 if hasattr(sel, "min_points") else P.n_monomials(spec.degree, src.shape[1])
+    nnz = [0]
+
+    def step(marks):
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((name, e))
+
+        mark("start")
+        bs, bt = D.device_bboxes([src_d, tgt_d])
+        cloud = D.SourceCloud(src_d, bbox=bs)
+        dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, P._r_max_device(cloud, tgt_d, bt)) \
+            if hasattr(sel, "min_points") else D.fixed(sel.r_c)
+        mark("grid")
+        ops, checks = D.map_chunked(cloud, tgt_d, dsel, rbf, spec.degree, spec.lam,
+                                    spec.centering, X_d, Y, meta["chunk"],
+                                    keep=meta["applies"] > 1, min_required=need)
+        nnz[0] = sum(o.nnz for _, _, o in ops) if ops else nnz[0]
+        mark("map")
+        for t in range(meta["applies"] - 1):  # the remaining timesteps' applies
+            for c0, c1, op in ops:
+                op.apply(X_d, out=Y[c0:c1])
+        if meta["applies"] > 1:
+            mark("applies")
+        out = Y
+        if meta["gather"] and world > 1:
+            out = gather_target_field(Y, nt * world)
+            mark("allgather")
+        return out, checks, cloud
+
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        sampler.wait_first_sample()
+        for _ in range(args.warmup):
+            out, checks, cloud = step([])
+        torch.cuda.synchronize()
+        bad = [(c0, int(st[0].item())) for c0, sst, st in checks if int(st[0].item())]
+        if any(sst[2] or sst[4] for _, sst, _ in checks) or bad:
+            raise SystemExit(f"selection/fit failures in the benchmark workload: {bad}")
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler.mark_timed()
+        phase, total = {}, 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            marks = []
+            out, checks, cloud = step(marks)
+            torch.cuda.synchronize()
+            for (a, ea), (b, eb) in zip(marks[:-1], marks[1:]):
+                phase[b] = phase.get(b, 0.0) + ea.elapsed_time(eb)
+            total += marks[0][1].elapsed_time(marks[-1][1])
+    t = torch.tensor([total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    value = meta["total"] * args.steps / (total * 1e-3)
+    # sampled parity (outside the timed region): oracle on a uniform stride of
+    # this rank's targets against the whole source set
+    par = None
+    if not args.no_parity and rank == 0:
+        from oracle import parity
+
+        from paper_2510_18838_b200.pointwise import _KIND_CODE
+
+        stride = max(1, nt // args.parity_sample)
+        idx = np.arange(0, nt, stride)
+        ts = np.ascontiguousarray(tgt[idx])
+        tsd = D.to_device(ts)
+        cl = D.SourceCloud(src_d, bbox=D.device_bboxes([src_d])[0])
+        dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, P._r_max_device(cl, tgt_d)) \
+            if hasattr(sel, "min_points") else D.fixed(sel.r_c)
+        sl = D.select(cl, tsd, dsel, cl.target_order(tsd), need)
+        off, sid, dist_, _w = D.support_csr(cl, tsd, sl)
+        dev = {"off": off.cpu().numpy(), "idx": sid.cpu().numpy(), "dist": dist_.cpu().numpy(),
+               "values": Y.cpu().numpy()[idx]}
+        if sl.radii is not None:
+            dev["radii"] = sl.radii.cpu().numpy()
+            dev["status"] = sl.status.cpu().numpy()
+        # r_max of the whole rank's target set (as the device run used)
+        osel = ("adaptive", sel.min_points, sel.r0, sel.growth) if hasattr(sel, "min_points") \
+            else ("fixed", sel.r_c)
+        ref = parity.oracle_transfer(src, X, ts, spec.degree, _KIND_CODE[spec.rbf.kind],
+                                     spec.rbf.a, osel, spec.lam, spec.centering,
+                                     r_max=P._r_max(src, tgt) if hasattr(sel, "min_points")
+                                     else None)
+        par = parity.check_transfer(src, X, ts, spec.degree, _KIND_CODE[spec.rbf.kind],
+                                    spec.rbf.a, osel, dev, spec.lam, spec.centering, ref=ref)
+        par["sample"] = f"every {stride}-th of this rank's {nt} targets ({idx.size})"
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": value, "unit": "targets/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps,
+        "higher_is_better": True, "scaling": meta["scaling"], "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded uniform clouds / tensor grid)",
+        "config": bench_config(desc, world),
+        "phases_ms_per_step": {k: v / args.steps for k, v in phase.items()},
+        "nnz_per_rank": nnz[0] or None, "parity": par, "clocks": sampler.summary(),
+        "e2e": None, "cpu_baseline": None,
+    }
+
+
 # ------------------------------------------------------- reference arm
 _REF = {}  # state shared with forked workers (set before the fork, never pickled)
 
@@ -679,7 +889,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=["c1", "c2", "lattice1m"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "lattice1m", "c3", "c3mq", "c4", "c5"],
+                    default="c2")
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="c3/c4/c5: shrink the point counts by this factor (checks)")
+    ap.add_argument("--parity-sample", type=int, default=20000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -700,7 +914,7 @@ def main():
 
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = run_b200(args, rank, world, local_rank)
+        line = (run_large if args.config in LARGE else run_b200)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
 

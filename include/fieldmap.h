@@ -189,6 +189,14 @@ int fm_support_fill(const fm_grid *grid, const int32_t *cell_start, const double
                     const int64_t *offsets, int32_t max_count, int64_t *idx, double *dist,
                     const fm_rbf *rbf, double *w, fm_stream_t stream);
 
+/* Per-axis metric (an extension; the reference is isotropic): out[i, a] =
+ * pts[i, a] * scale_host[a], (n, dim) row-major, device in/out.  Scaling
+ * sources and targets alike turns the isotropic radius search and fit into
+ * the anisotropic metric diag(scale) (e.g. spatial x velocity axes of a 5-D
+ * distribution function; SURVEY.md §7 decision 6). */
+int fm_scale_points(const double *pts, int64_t n, int32_t dim, const double *scale_host,
+                    double *out, fm_stream_t stream);
+
 /* ------------------------------------------------- a5: radial weights
  * rbf_weights(kind, a, r_c, r) (_ext.pyx:65-75). */
 int fm_rbf_weights(int kind, double a, double r_c, const double *r, int64_t n, double *out,

@@ -52,7 +52,7 @@ def cond_of_fit(src, target, idx, w, degree, centering=True):
 
 
 def oracle_transfer(src, X, tgt, degree, kind, a, selection, lam=0.0, centering=True,
-                    nthreads=None):
+                    nthreads=None, r_max=None):
     """The reference path on the host (see module docstring).  Returns a dict
     with off/idx/dist[/radii/status], w, values (nt, C), fit_status."""
     nthreads = nthreads or os.cpu_count() or 1
@@ -66,9 +66,9 @@ def oracle_transfer(src, X, tgt, degree, kind, a, selection, lam=0.0, centering=
         radius = float(selection[1])
     else:
         _, min_pts, r0, growth = selection
+        rm = O.r_max_for(src, tgt) if r_max is None else float(r_max)
         off, idx, dist, radii, st = O.supports_nd(
-            tgt, grid, (int(min_pts), float(r0), float(growth), O.r_max_for(src, tgt)),
-            nthreads)
+            tgt, grid, (int(min_pts), float(r0), float(growth), rm), nthreads)
         out.update(radii=radii, status=st)
         radius = radii
     w = np.abs(O.rbf_for_supports(kind, a, off, dist, radius))

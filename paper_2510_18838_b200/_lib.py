@@ -79,6 +79,7 @@ SIGNATURES = {
     "fm_support_fill": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
                                 c_vp, c_vp, c_i32, c_vp, c_vp, P(FmRbf), c_vp, c_vp]),
     "fm_rbf_weights": (c_i32, [c_i32, c_dbl, c_dbl, c_vp, c_i64, c_vp, c_vp]),
+    "fm_scale_points": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "fm_fit_many": (c_i32, [P(FmFit), c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                             c_vp, c_vp, c_vp, c_vp]),
     "fm_select_supports": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),

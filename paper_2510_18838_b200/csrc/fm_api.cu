@@ -17,6 +17,22 @@ __global__ void k_rbf(int kind, double a, double r_c, const double *__restrict__
         out[i] = rbf_one(kind, a, r_c, r[i]);
 }
 
+// ------------------------------------------------- per-axis metric
+// out[i, a] = pts[i, a] * scale[a]: the per-axis coordinate scaling of an
+// anisotropic metric (SURVEY.md §7 decision 6), applied to sources and
+// targets before the isotropic search and fit (IEEE products, so a host
+// oracle scaling the same way sees bit-identical coordinates)
+struct Scale5 {
+    double s[kMaxDim];
+};
+__global__ void k_scale_points(const double *__restrict__ pts, int64_t n, int dim, Scale5 sc,
+                               double *__restrict__ out) {
+    const int64_t total = n * dim;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __dmul_rn(pts[i], sc.s[i % dim]);
+}
+
 // -------------------------------------------------------------- apply
 // Y[row_target[k], :] = sum_j val[j] * X[col[j], :] over stored row k.
 // Rows are stored in processing (cell) order, so a warp's tile of 32/L
@@ -258,6 +274,19 @@ int fm_support_fill(const fm_grid *grid, const int32_t *cell_start, const double
     case 4: return dim4_fill(s, offsets, max_count, idx, dist, kind, a, w, st);
     default: return dim5_fill(s, offsets, max_count, idx, dist, kind, a, w, st);
     }
+}
+
+int fm_scale_points(const double *pts, int64_t n, int32_t dim, const double *scale_host,
+                    double *out, fm_stream_t stream) {
+    if (n < 0 || dim < 1 || dim > kMaxDim || !scale_host) return FM_ERR_ARG;
+    if (n == 0) return FM_OK;
+    Scale5 sc{};
+    for (int a = 0; a < dim; a++) sc.s[a] = scale_host[a];
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((n * dim + threads - 1) / threads, (int64_t)kSMs * 16);
+    k_scale_points<<<blocks, threads, 0, (cudaStream_t)stream>>>(pts, n, dim, sc, out);
+    FM_CHECK_LAUNCH();
+    return FM_OK;
 }
 
 int fm_rbf_weights(int kind, double a, double r_c, const double *r, int64_t n, double *out,

@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kBlock, G == 8 ? 8 : 1) k_select(SearchArgs s,
 // Thread-per-target select pass (1-D / 2-D): same outputs as k_select.
 // The supports go from the per-thread shared-memory lists to the slots with
 // one coalesced warp store per target (lanes over entries).
-constexpr int kThreadListCap = 48;  // 8 CTAs/SM: 8 x 25 KB of lists
+constexpr int kThreadListCap = 48;  // default 2-D slot: 8 CTAs/SM of 25 KB lists
 
 template <int DIM>
 __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t min_required, int lcap,
@@ -895,8 +895,10 @@ int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, do
     constexpr int G = DIM <= 2 ? 8 : 16;
     k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0);
     if (s.nt == 0) return FM_OK;
-    if (DIM <= 2 && !select_groups_forced()) {
-        const int lcap = slot_cap < kThreadListCap ? slot_cap : kThreadListCap;
+    if (DIM <= 2 && slot_cap <= 2 * kThreadListCap && !select_groups_forced()) {
+        // the per-thread list IS the slot: a position is slotted iff its
+        // support fits slot_cap (what the size buckets and the build assume)
+        const int lcap = slot_cap;
         const size_t sm = (size_t)kBlock * (lcap | 1) * sizeof(int32_t);
         if (sm > 48 * 1024)
             cudaFuncSetAttribute(k_select_t<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -264,7 +264,9 @@ def fit_many(targets, sup_off, sup_idx, sup_w, src, src_val, degree, lam, center
 def slot_capacity(dim, sel):
     """Per-target slot size of the select pass (overflowing supports are
     re-gathered by the build, so this is a speed knob, not a limit)."""
-    base = 64 if dim <= 2 else (128 if dim == 3 else 256)
+    if dim <= 2:
+        return 48  # the thread-per-target select's list (k_select_t): 8 CTAs per SM
+    base = 128 if dim == 3 else 256
     if sel.adaptive:
         est = int(np.ceil(sel.min_pts * sel.growth ** dim * 1.25))
         base = max(base, min(256, -(-est // 32) * 32))
@@ -455,6 +457,43 @@ def build_operator(cloud, targets, sl, rbf, degree, lam, centering):
                               ctypes.byref(f), ptr(col), ptr(val), ptr(status), ptr(stats),
                               _stream()), "fm_build_operator")
     return Operator(sl.offsets, col, val, status, sl.perm, cloud.n), stats
+
+
+def scale_points(pts, scale):
+    """Per-axis metric: pts * scale (fm_scale_points, device in/out)."""
+    sc = np.ascontiguousarray(scale, dtype=np.float64)
+    if sc.shape != (pts.shape[1],):
+        raise ValueError(f"metric needs {pts.shape[1]} per-axis scales, got {sc.shape}")
+    out = torch.empty_like(pts)
+    check(_lib.lib().fm_scale_points(ptr(pts), pts.shape[0], pts.shape[1], sc.ctypes.data,
+                                     ptr(out), _stream()), "fm_scale_points")
+    return out
+
+
+def map_chunked(cloud, targets, sel, rbf, degree, lam, centering, X, Y, chunk, keep=False,
+                min_required=0, on_chunk=None):
+    """The whole path for `targets` in chunks of `chunk` (bounded scratch:
+    slots and records exist for one chunk at a time): per chunk, target order,
+    select, operator build, apply of X (ns, C) into Y[c0:c1].  Returns the
+    chunks' operators when `keep` (repeated applies), and the per-chunk
+    (select stats, fit stats) for error reporting."""
+    nt = int(targets.shape[0])
+    X2 = X.reshape(X.shape[0], -1)
+    ops, checks = [], []
+    for c0 in range(0, nt, max(1, int(chunk))):
+        c1 = min(nt, c0 + int(chunk))
+        tb = targets[c0:c1]
+        perm = cloud.target_order(tb)
+        sl = select(cloud, tb, sel, perm, min_required)
+        op, st = build_operator(cloud, tb, sl, rbf, degree, lam, centering)
+        op.apply(X2, out=Y[c0:c1])
+        checks.append((c0, sl.stats.copy(), st))
+        if keep:
+            ops.append((c0, c1, op))
+        if on_chunk is not None:
+            on_chunk(c0, c1, sl, op)
+        del sl
+    return ops, checks
 
 
 def fp64_probe(blocks=148 * 8, threads=256, iters=4096):

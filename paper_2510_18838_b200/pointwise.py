@@ -411,6 +411,22 @@ class _Plan:
                                  fs.degree, fs.lam, fs.centering)
 
 
+def _apply_metric(points, metric):
+    """Per-axis metric (extension, SURVEY.md §7 decision 6): coordinates
+    scaled by `metric` (one factor per axis) -- numpy on the host, tensors on
+    the device (fm_scale_points); the same IEEE products either way."""
+    if metric is None:
+        return points
+    if isinstance(points, torch.Tensor):
+        pts = D.to_device(points)
+        return D.scale_points(pts.reshape(pts.shape[0], -1), metric)
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    sc = np.asarray(metric, dtype=np.float64)
+    if pts.ndim != 2 or sc.shape != (pts.shape[1],):
+        raise ValueError(f"metric needs one scale per axis ({pts.shape[-1]}), got {sc.shape}")
+    return np.ascontiguousarray(pts * sc)
+
+
 def _as_points(a, dim=None):
     arr = np.ascontiguousarray(a, dtype=np.float64)
     if dim is not None:
@@ -478,7 +494,13 @@ class PreparedTransfer:
     Fit failures are reported by `apply`, like the reference's."""
 
     def __init__(self, source_points, target_points, fitspec, grid=None, mesh=None,
-                 source_location="vertices"):
+                 source_location="vertices", metric=None):
+        if metric is not None:  # extension: anisotropic (per-axis) metric
+            dim = (source_points.shape[1] if getattr(source_points, "ndim", 1) == 2 else 2)
+            source_points = _apply_metric(source_points, metric)
+            target_points = _apply_metric(
+                target_points.reshape(-1, dim) if isinstance(target_points, torch.Tensor)
+                else np.asarray(target_points, dtype=np.float64).reshape(-1, dim), metric)
         if isinstance(source_points, torch.Tensor):
             # device-resident inputs: CUDA tensors in, nothing copied to the host
             self.src_xy = D.to_device(source_points)
@@ -549,13 +571,20 @@ class PreparedTransfer:
 
 
 def fit_point_cloud(source_points, source_values, target_points, fitspec, grid=None, mesh=None,
-                    source_location="vertices", threads=1):
+                    source_location="vertices", threads=1, metric=None):
     """Fit a value at each target from a scattered source point cloud
     (pointwise.py:434-451).  numpy in -> numpy out.  torch tensors in: CUDA
     tensors -> CUDA tensor out (nothing copied to the host); host tensors
     (pinned: asynchronous copies) -> pinned host tensor out, with the field's
     host->device copy on a side stream overlapping the whole selection and
-    operator build."""
+    operator build.  `metric` (extension): per-axis coordinate scales of an
+    anisotropic metric, applied to sources and targets before the search."""
+    if metric is not None:
+        dim = source_points.shape[1] if getattr(source_points, "ndim", 1) == 2 else 2
+        source_points = _apply_metric(source_points, metric)
+        target_points = _apply_metric(
+            target_points.reshape(-1, dim) if isinstance(target_points, torch.Tensor)
+            else np.asarray(target_points, dtype=np.float64).reshape(-1, dim), metric)
     if any(isinstance(a, torch.Tensor) for a in (source_points, source_values, target_points)):
         return _fit_point_cloud_tensors(source_points, source_values, target_points, fitspec,
                                         grid, mesh, source_location)

@@ -905,3 +905,62 @@ def test_map_gathered_blocks_equal_one_shot():
             assert torch.equal(got, want), nb
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_per_axis_metric_5d_vs_oracle():
+    """Extension (SURVEY §7 decision 6): fit_point_cloud(metric=...) equals
+    the oracle run on the per-axis scaled coordinates (5-D tensor grid, degree
+    1, adaptive), bitwise supports through PreparedTransfer.support."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2510_18838_b200 import pointwise as P
+
+    axes = [np.linspace(0, 1, k) for k in (9, 9, 5, 5, 5)]
+    g = np.meshgrid(*axes, indexing="ij")
+    src = np.ascontiguousarray(np.stack([a.reshape(-1) for a in g], axis=1))
+    tgt = np.random.RandomState(4).uniform(0, 1, (3000, 5))
+    metric = [1.0, 1.0, 0.5, 0.5, 0.5]
+    f = np.exp(-np.sum((src[:, 2:] - 0.5) ** 2, axis=1) * 4) * (1 + 0.1 * np.sin(3 * src[:, 0]))
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.AdaptiveRadius(12, 0.125, 1.5))
+    got = P.fit_point_cloud(src, f, tgt, spec, metric=metric)
+    ss, ts = src * np.asarray(metric), tgt * np.asarray(metric)
+    want, st, (off, idx, dist, w) = O.transfer(ss, f, ts, 1, O.RBF_C4, 2.0,
+                                               ("adaptive", 12, 0.125, 1.5))
+    assert (st == 0).all()
+    assert np.max(np.abs(got - want) / np.abs(want)) < 1e-10
+    pt = P.PreparedTransfer(src, tgt, spec, metric=metric)
+    off2, idx2, _w = pt.support
+    assert np.array_equal(off2, off) and np.array_equal(idx2, idx)
+    # device tensors in: same values
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    got_t = P.fit_point_cloud(d(src), d(f), d(tgt), spec, metric=metric).cpu().numpy()
+    assert np.array_equal(got_t, got)
+
+
+@pytest.mark.gpu
+def test_map_chunked_equals_one_shot():
+    """device.map_chunked (bounded scratch for C4/C5-size target sets) gives
+    bitwise the one-shot operator's values, for 3-D degree 3 (k = 20)."""
+    import torch
+
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+
+    src = np.random.RandomState(1).uniform(0, 1, (20000, 3))
+    tgt = np.random.RandomState(5).uniform(0, 1, (7000, 3))
+    f = (np.sin(3 * src[:, 0]) * np.cos(2 * src[:, 1]) * np.exp(src[:, 2]) + 2.0)[:, None]
+    spec = P.FitSpec(3, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
+                     P.AdaptiveRadius(40, 20000 ** (-1 / 3), 1.5))
+    want = P.fit_point_cloud(src, f, tgt, spec)
+    src_d, tgt_d, X_d = D.to_device(src), D.to_device(tgt), D.to_device(f)
+    bs, bt = D.device_bboxes([src_d, tgt_d])
+    cloud = D.SourceCloud(src_d, bbox=bs)
+    sel = spec.selection
+    dsel = D.adaptive(sel.min_points, sel.r0, sel.growth, P._r_max_device(cloud, tgt_d, bt))
+    Y = torch.empty((7000, 1), dtype=torch.float64, device="cuda")
+    ops, checks = D.map_chunked(cloud, tgt_d, dsel, P._rbf_pair(spec.rbf), 3, 0.0, True, X_d, Y,
+                                2500, keep=True)
+    assert len(ops) == 3 and all(int(st[0].item()) == 0 for _, _, st in checks)
+    assert np.array_equal(Y.cpu().numpy(), want)

@@ -41,12 +41,13 @@ def _device_run(src, X, tgt, spec, slot_cap=None):
         dsel = D.fixed(s.r_c)
         osel = ("fixed", s.r_c)
     sl = D.select(cloud, tgt_d, dsel, perm, 0, slot_cap=slot_cap)
-    op, _stats = D.build_operator(cloud, tgt_d, sl, P._rbf_pair(spec.rbf), spec.degree,
-                                  spec.lam, spec.centering)
+    op, stats = D.build_operator(cloud, tgt_d, sl, P._rbf_pair(spec.rbf), spec.degree,
+                                 spec.lam, spec.centering)
     Y = op.apply(D.to_device(X))
     off, idx, dist, _w = D.support_csr(cloud, tgt_d, sl)
     dev = {"off": off.cpu().numpy(), "idx": idx.cpu().numpy(), "dist": dist.cpu().numpy(),
-           "values": Y.cpu().numpy(), "fit_status": op.status.cpu().numpy()}
+           "values": Y.cpu().numpy(), "fit_status": op.status.cpu().numpy(),
+           "fail_count": int(stats[0].item())}
     if sl.radii is not None:
         dev["radii"] = sl.radii.cpu().numpy()
         dev["status"] = sl.status.cpu().numpy()
@@ -54,7 +55,9 @@ def _device_run(src, X, tgt, spec, slot_cap=None):
     return dev, osel, sl
 
 
-def _assert_parity(r):
+def _assert_parity(r, dev=None):
+    if dev is not None:  # the build's failure count (what the API raises on) agrees
+        assert dev["fail_count"] == r["fit_failures"], (dev["fail_count"], r)
     assert r["supports_bitwise"], r
     assert r.get("radii_bitwise", True), r
     assert r.get("select_status_equal", True), r
@@ -75,7 +78,7 @@ def test_c2_full_scale_vs_oracle():
     r = parity.check_transfer(src, X, tgt, 2, O.RBF_C4, 2.0, osel, dev, rtol=VALUE_RTOL)
     print(r)
     assert r["nnz"] == 17478625
-    _assert_parity(r)
+    _assert_parity(r, dev)
 
 
 @pytest.mark.parametrize("slot_cap", [None, 24])
@@ -100,5 +103,5 @@ def test_random_2m_gaussian_multiquadric_vs_oracle(slot_cap):
                                   rtol=VALUE_RTOL, ref=ref)
         print(kind, r)
         assert np.diff(dev["off"]).max() >= 48
-        _assert_parity(r)
+        _assert_parity(r, dev)
         torch.cuda.empty_cache()
