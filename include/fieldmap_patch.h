@@ -32,9 +32,14 @@ extern "C" {
  * permutation of 0..nt-1, or NULL) is the processing order -- e.g. targets
  * sorted by seed element, for L2 locality; outputs stay at each target's own
  * position, so results never depend on it.
- *   fm_patch_count: counts int64 (nt) (-1 on overflow).
+ *   fm_patch_count: counts int64 (nt); -1 when the patch exceeds the bounds
+ *                   above, -2 when seed[i] is not an element id (e.g. -1, the
+ *                   not-found value of fm_locate_batch).  A caller must stop on
+ *                   any negative count (Python raises FieldmapError /
+ *                   InsufficientSourcesError) before scanning the counts.
  *   fm_patch_fill:  idx int64 at off[i] .. off[i+1] (off = exclusive scan of
- *                   counts, int64 (nt+1)).  Bitwise equal to the reference. */
+ *                   the counts, int64 (nt+1)); targets with a negative count
+ *                   write nothing.  Bitwise equal to the reference. */
 int fm_patch_count(const int64_t *seed, int64_t nt, const int64_t *order, const int32_t *adj_off,
                    const int32_t *adj, const int32_t *tris, int64_t ne, int32_t layers,
                    int32_t centroids, int64_t *counts, fm_stream_t stream);

@@ -160,6 +160,8 @@ def patch_supports(seed, tris, edge_tris, layers, centroids):
     counts = counts.cpu().numpy()
     if (counts < 0).any():
         i = int(np.argmax(counts < 0))
+        if counts[i] == -2:
+            raise ValueError(f"seed of target {i} is not an element id (not located?)")
         raise FieldmapError(f"element patch of target {i} exceeds the kernel's per-target "
                             "bound (FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)")
     return off.cpu().numpy(), idx.cpu().numpy(), counts

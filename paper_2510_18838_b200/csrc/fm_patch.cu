@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(128)
     k_patch(const int64_t *__restrict__ seed, int64_t nt, const int64_t *__restrict__ order,
             const int32_t *__restrict__ adj_off, const int32_t *__restrict__ adj,
             const int32_t *__restrict__ tris, int32_t layers,
-            int32_t centroids, int64_t *__restrict__ counts, const int64_t *__restrict__ off,
-            int64_t *__restrict__ idx) {
+            int32_t centroids, int64_t ne, int64_t *__restrict__ counts,
+            const int64_t *__restrict__ off, int64_t *__restrict__ idx) {
     int32_t el[FM_PATCH_MAX_ELEMS];
     int32_t dof[FM_PATCH_MAX_DOFS];
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nt;
@@ -34,7 +34,12 @@ __global__ void __launch_bounds__(128)
         const int64_t i = order ? __ldg(order + p) : p;
         int n = 1;
         bool overflow = false;
-        el[0] = (int32_t)__ldg(seed + i);
+        const int64_t sd = __ldg(seed + i);
+        if (sd < 0 || sd >= ne) {  // not located (-1) or not an element: no patch
+            if (!FILL) counts[i] = -2;
+            continue;
+        }
+        el[0] = (int32_t)sd;
         int fs = 0, fe = 1;  // frontier [fs, fe)
         for (int layer = 0; layer < layers && !overflow && fs < fe; layer++) {
             for (int f = fs; f < fe && !overflow; f++) {
@@ -120,10 +125,10 @@ static int launch_patch(bool fill, const int64_t *seed, int64_t nt, const int64_
     const int blocks = (int)std::min<int64_t>((nt + threads - 1) / threads, (int64_t)kSMs * 16);
     if (fill)
         k_patch<true><<<blocks, threads, 0, stream>>>(seed, nt, order, adj_off, adj, tris,
-                                                      layers, centroids, nullptr, off, idx);
+                                                      layers, centroids, ne, nullptr, off, idx);
     else
         k_patch<false><<<blocks, threads, 0, stream>>>(seed, nt, order, adj_off, adj, tris,
-                                                       layers, centroids, counts, nullptr,
+                                                       layers, centroids, ne, counts, nullptr,
                                                        nullptr);
     FM_CHECK_LAUNCH();
     return FM_OK;

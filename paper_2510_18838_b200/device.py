@@ -573,19 +573,70 @@ def patch_supports(topo, seed, layers, centroids, sort_by_seed=None):
     return offsets, idx, counts
 
 
-def locate_elements(eg, mesh, pts, tol=1e-10):
+class MeshDevice:
+    """A triangle mesh's arrays resident in HBM, uploaded once per mesh: what
+    fm_locate_batch reads (tri_xy, tris, tri_edges, vert_gid, tri_gid, inv2a,
+    epsfac), the element grid, and the patch adjacency (PatchTopology) --
+    reused by every batch of transfer_extrinsic and every apply."""
+
+    def __init__(self, mesh):
+        f64 = lambda a: to_device(a, torch.float64)  # noqa: E731
+        i64 = lambda a: to_device(  # noqa: E731
+            a if isinstance(a, torch.Tensor) else np.array(a, dtype=np.int64), torch.int64)
+        self.arrays = [f64(mesh.tri_xy), i64(mesh.tris), i64(mesh.tri_edges),
+                       i64(mesh.vert_gid), i64(mesh.tri_gid), f64(mesh.inv2a), f64(mesh.epsfac)]
+        self._grid = None
+        self._topo = None
+        self.mesh = mesh
+
+    def grid(self):
+        if self._grid is None:
+            from .locate import ElementGrid
+
+            self._grid = ElementGrid(self.mesh)
+        return self._grid
+
+    def topology(self):
+        if self._topo is None:
+            self._topo = PatchTopology.from_mesh_arrays(self.mesh.tris, self.mesh.edge_tris)
+        return self._topo
+
+
+_MESHES = {}
+
+
+def mesh_device(mesh):
+    """The MeshDevice of `mesh`, cached on the mesh object (or, when it takes
+    no attributes, in a small per-process table that keeps the mesh alive)."""
+    md = getattr(mesh, "_fm_device", None)
+    if isinstance(md, MeshDevice) and md.mesh is mesh:
+        return md
+    md = MeshDevice(mesh)
+    try:
+        mesh._fm_device = md
+    except (AttributeError, TypeError):
+        if len(_MESHES) >= 8:
+            _MESHES.pop(next(iter(_MESHES)))
+        _MESHES[id(mesh)] = md
+        md = _MESHES[id(mesh)]
+    return md
+
+
+def locate_elements(eg, mesh, pts, tol=1e-10, md=None):
     """fm_locate_batch on device points over an element grid (the caller's
     locate_arrays, locate.py:175-186, DEFAULT_TOL 1e-10 at locate.py:28):
-    (found u8, elem int64) device tensors."""
+    (found u8, elem int64) device tensors.  The mesh arrays come from its
+    MeshDevice (uploaded once)."""
     L = _lib.lib()
     n = int(pts.shape[0])
     dev = pts.device
-    f64 = lambda a: to_device(a, torch.float64)  # noqa: E731
+    md = md or mesh_device(mesh)
+    arrs = md.arrays
     i64 = lambda a: to_device(  # noqa: E731
         a if isinstance(a, torch.Tensor) else np.array(a, dtype=np.int64), torch.int64)
-    arrs = [f64(mesh.tri_xy), i64(mesh.tris), i64(mesh.tri_edges), i64(mesh.vert_gid),
-            i64(mesh.tri_gid), f64(mesh.inv2a), f64(mesh.epsfac)]
-    cell_off, cell_items = i64(eg.cell_offsets), i64(eg.cell_items)
+    if getattr(eg, "_dev_csr", None) is None:
+        eg._dev_csr = (i64(eg.cell_offsets), i64(eg.cell_items))
+    cell_off, cell_items = eg._dev_csr
     found = _empty(n, torch.uint8, dev)
     elem = _empty(n, torch.int64, dev)
     dim = _empty(n, torch.int64, dev)

@@ -258,17 +258,17 @@ class _PatchSupports:
     reference's, naming the first failing target."""
 
     def __init__(self, targets, fitspec, mesh, source_location, grid=None, base_index=0):
-        from .locate import ElementGrid
-
         if targets.shape[1] != 2:
             raise FieldError("element-patch selection is 2-D (triangle meshes)")
-        if grid is not None and getattr(grid, "mesh", None) is mesh and hasattr(
-                grid, "cell_items") and not isinstance(grid, PointGrid):
+        md = D.mesh_device(mesh)  # mesh arrays, element grid, adjacency: uploaded once
+        if grid is not None and hasattr(grid, "cell_items") and not isinstance(grid, PointGrid):
+            if getattr(grid, "mesh", None) is not mesh:
+                raise ValueError("grid was built for a different mesh")  # locate.py:177-178
             eg = grid
         else:
-            eg = ElementGrid(mesh)
+            eg = md.grid()
         t = D.to_device(targets)
-        found, elem = D.locate_elements(eg, mesh, t)
+        found, elem = D.locate_elements(eg, mesh, t, md=md)
         found_h = found.cpu().numpy()
         if not found_h.all():
             i = int(np.argmax(~found_h))
@@ -276,20 +276,27 @@ class _PatchSupports:
                 f"{_point_label(targets, i)} (index {base_index + i}) lies "
                 "outside the source mesh; element-patch selection needs a "
                 "containing element")
-        topo = D.PatchTopology.from_mesh_arrays(mesh.tris, mesh.edge_tris)
+        topo = md.topology()
         self.offsets, self.idx, counts = D.patch_supports(
             topo, elem, fitspec.selection.layers, source_location == "centroids")
         counts_h = counts.cpu().numpy()
-        if (counts_h < 0).any():
-            from ._lib import FieldmapError
-
-            i = int(np.argmax(counts_h < 0))
-            raise FieldmapError(
-                f"{_point_label(targets, i)} (index {base_index + i}): element patch exceeds "
-                "the kernel's per-target bound (FM_PATCH_MAX_ELEMS / FM_PATCH_MAX_DOFS)")
         need = n_monomials(fitspec.degree)
-        if (counts_h < need).any():
-            i = int(np.argmax(counts_h < need))
+        bad = (counts_h < 0) | (counts_h < need)
+        if bad.any():
+            # the first failing target in index order, as the reference's
+            # per-target loop raises (pointwise.py:276-296)
+            i = int(np.argmax(bad))
+            if counts_h[i] == -2:  # seed is not an element (not located)
+                raise InsufficientSourcesError(
+                    f"{_point_label(targets, i)} (index {base_index + i}) lies outside the "
+                    "source mesh; element-patch selection needs a containing element")
+            if counts_h[i] < 0:
+                from ._lib import FieldmapError
+
+                raise FieldmapError(
+                    f"{_point_label(targets, i)} (index {base_index + i}): element patch "
+                    "exceeds the kernel's per-target bound (FM_PATCH_MAX_ELEMS / "
+                    "FM_PATCH_MAX_DOFS)")
             raise UnderdeterminedError(
                 f"{_point_label(targets, i)} (index {base_index + i}) patch "
                 f"has {counts_h[i]} dofs; a degree-{fitspec.degree} fit needs "
@@ -305,8 +312,12 @@ class _PatchSupports:
         return (self.offsets.cpu().numpy(), self.idx.cpu().numpy(), self.w.cpu().numpy())
 
     def values(self, src_xy, src_vals):
-        """_fit_batch (pointwise.py:299-314) per component on the patch CSR."""
-        src = D.to_device(src_xy)
+        """_fit_batch (pointwise.py:299-314) per component on the patch CSR.
+        The source coordinates stay on the device between calls (same array)."""
+        if getattr(self, "_src_key", None) is not src_xy:
+            self._src_d = D.to_device(src_xy)
+            self._src_key = src_xy
+        src = self._src_d
         vals = D.to_device(src_vals)
         cols = vals.reshape(vals.shape[0], -1)
         out = []
@@ -723,10 +734,9 @@ def _transfer_extrinsic_patch(evaluate_callback, targets, fitspec, src_xy, batch
     """transfer_extrinsic's batch loop (pointwise.py:488-510) with ElementPatch
     selection: per batch, locate + patch supports on the device, one callback
     for the batch's distinct dofs, the fit on the device."""
-    from .locate import ElementGrid
 
     nt = targets.shape[0]
-    eg = ElementGrid(mesh)
+    eg = D.mesh_device(mesh).grid()  # built once, reused by every batch
     out = np.empty(nt, dtype=np.float64)
     values_cache = np.full(src_xy.shape[0], np.nan, dtype=np.float64)
     for bi, b0 in enumerate(range(0, nt, batch_size)):

@@ -694,6 +694,10 @@ def test_patch_supports_random_seeds_and_overflow():
     assert off.tolist() == [0] and idx.size == 0
     with pytest.raises(FieldmapError):
         Kb.patch_supports(seeds[:10], tris, et, 12, True)
+    # locate's not-found seed (-1) and out-of-range ids are rejected, not read
+    for bad in (-1, tris.shape[0]):
+        with pytest.raises(ValueError):
+            Kb.patch_supports(np.array([3, bad, 5]), tris, et, 2, False)
 
 
 @pytest.mark.gpu
