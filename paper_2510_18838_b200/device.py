@@ -42,6 +42,8 @@ def to_device(a, dtype=torch.float64):
         # host tensor: pinned memory makes this an async H2D copy on the stream
         return a.to(dtype=dtype).contiguous().to(_dev(), non_blocking=a.is_pinned())
     arr = np.ascontiguousarray(a, dtype=np.float64 if dtype == torch.float64 else None)
+    if not arr.flags.writeable:  # torch.from_numpy wants a writable buffer
+        arr = arr.copy()
     return torch.from_numpy(arr).to(_dev(), non_blocking=False)
 
 
