@@ -47,6 +47,23 @@ int fm_patch_fill(const int64_t *seed, int64_t nt, const int64_t *order, const i
                   const int32_t *adj, const int32_t *tris, int64_t ne, int32_t layers,
                   int32_t centroids, const int64_t *off, int64_t *idx, fm_stream_t stream);
 
+/* Targets whose patch exceeds the bounds above (count -1) have no size limit
+ * the reference lacks: the same patch with element / dof lists of capacity
+ * max_elems / max_dofs in caller scratch (fm_patch_big_workspace bytes), for
+ * the targets list[0..nlist) only; counts[list[p]] is overwritten (still -1
+ * if even these capacities are exceeded), fill writes at off[list[p]]. */
+size_t fm_patch_big_workspace(int64_t nlist, int32_t max_elems, int32_t max_dofs);
+int fm_patch_count_big(const int64_t *seed, const int64_t *list, int64_t nlist,
+                       const int32_t *adj_off, const int32_t *adj, const int32_t *tris, int64_t ne,
+                       int32_t layers, int32_t centroids, int32_t max_elems, int32_t max_dofs,
+                       void *workspace, size_t workspace_bytes, int64_t *counts,
+                       fm_stream_t stream);
+int fm_patch_fill_big(const int64_t *seed, const int64_t *list, int64_t nlist,
+                      const int32_t *adj_off, const int32_t *adj, const int32_t *tris, int64_t ne,
+                      int32_t layers, int32_t centroids, int32_t max_elems, int32_t max_dofs,
+                      void *workspace, size_t workspace_bytes, const int64_t *off, int64_t *idx,
+                      fm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

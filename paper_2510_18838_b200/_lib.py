@@ -112,6 +112,11 @@ SIGNATURES = {
                                c_vp]),
     "fm_patch_fill": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp,
                               c_vp, c_vp]),
+    "fm_patch_big_workspace": (c_sz, [c_i64, c_i32, c_i32]),
+    "fm_patch_count_big": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32,
+                                   c_i32, c_vp, c_sz, c_vp, c_vp]),
+    "fm_patch_fill_big": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32,
+                                  c_i32, c_vp, c_sz, c_vp, c_vp, c_vp]),
     "fm_locate_batch": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64,
                                 c_f64, c_f64, c_f64, c_i64, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp,
                                 c_vp, c_vp, c_vp, c_vp]),

@@ -817,6 +817,12 @@ __global__ void __launch_bounds__(kBlock) k_fit_many(fm_fit fp, const double *__
     if (stats) warp_flush_pair(stats, nfail, first_fail);
 }
 
+}  // namespace fm
+
+#include "fm_big.cuh"
+
+namespace fm {
+
 // ------------------------------------------------------------ launchers
 inline int grid_blocks(int64_t nt, int groups_per_block, int per_sm) {
     const int64_t need = (nt + groups_per_block - 1) / groups_per_block;
@@ -988,6 +994,14 @@ int launch_build(const SearchArgs &s, const BuildArgs &b, int max_m, cudaStream_
     }
     if (need <= 256) return FM_BUILD(32, 8);
 #undef FM_BUILD
+    if constexpr (!FROM_SLOTS) {
+        // beyond 256 rows (only reached by re-gathered supports): the
+        // warp-per-target fit with the rows in global scratch
+        BigArgs g{};
+        g.klist = b.klist;
+        g.nk = b.nk;
+        return launch_fit_big<DIM, DEG, SOLVE, false>(s, b, g, need, st);
+    }
     return FM_ERR_UNSUPPORTED;
 }
 
@@ -1017,7 +1031,24 @@ int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const i
     }
     if (need <= 256) FM_FITMANY(32, 8);
 #undef FM_FITMANY
-    return FM_ERR_UNSUPPORTED;
+    // beyond 256 rows: warp per target, rows in global scratch (fm_big.cuh)
+    SearchArgs s{};
+    s.targets = targets;
+    s.nt = nt;
+    BuildArgs b{};
+    b.fp = fp;
+    b.src_val = src_val;
+    b.values = values;
+    b.status = status;
+    b.stats = stats;
+    BigArgs g{};
+    g.nk = nt;
+    g.sup_off = sup_off;
+    g.sup_idx = sup_idx;
+    g.sup_w = sup_w;
+    g.src = src;
+    g.coeffs = coeffs;
+    return launch_fit_big<DIM, DEG, true, true>(s, b, g, need, st);
 }
 
 // ------------------------------------------------- instantiation units

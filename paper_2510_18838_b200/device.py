@@ -24,6 +24,9 @@ from . import _lib
 from ._lib import FM_MAX_DIM, FmFit, FmGrid, FmLists, FmRbf, FmSelect, check, ptr
 
 INT32_MAX = 2 ** 31 - 1
+# capacities of the global-scratch patch path (targets beyond FM_PATCH_MAX_*)
+PATCH_BIG_ELEMS = 16384
+PATCH_BIG_DOFS = 32768
 
 
 def _stream():
@@ -567,11 +570,25 @@ def patch_supports(topo, seed, layers, centroids, sort_by_seed=None):
     args = (ptr(seed), nt, ptr(order), ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris), topo.ne,
             int(layers), int(bool(centroids)))
     check(L.fm_patch_count(*args, ptr(counts), _stream()), "fm_patch_count")
+    # patches beyond the per-thread bounds: again, with the element / dof lists
+    # in global scratch (no size limit the reference does not have)
+    big = torch.nonzero(counts == -1).reshape(-1) if nt else counts[:0]
+    nbig = int(big.shape[0])
+    bargs = None
+    if nbig:
+        ws_bytes = L.fm_patch_big_workspace(nbig, PATCH_BIG_ELEMS, PATCH_BIG_DOFS)
+        ws = _workspace(ws_bytes, seed.device)
+        bargs = (ptr(seed), ptr(big), nbig, ptr(topo.adj_off), ptr(topo.adj), ptr(topo.tris),
+                 topo.ne, int(layers), int(bool(centroids)), PATCH_BIG_ELEMS, PATCH_BIG_DOFS,
+                 ptr(ws), ws_bytes)
+        check(L.fm_patch_count_big(*bargs, ptr(counts), _stream()), "fm_patch_count_big")
     offsets = torch.zeros(nt + 1, dtype=torch.int64, device=seed.device)
     torch.cumsum(counts.clamp_min(0), 0, out=offsets[1:])
     nnz = int(offsets[-1]) if nt else 0
     idx = torch.empty(nnz, dtype=torch.int64, device=seed.device)
     check(L.fm_patch_fill(*args, ptr(offsets), ptr(idx), _stream()), "fm_patch_fill")
+    if nbig:
+        check(L.fm_patch_fill_big(*bargs, ptr(offsets), ptr(idx), _stream()), "fm_patch_fill_big")
     return offsets, idx, counts
 
 

@@ -678,10 +678,8 @@ def test_patch_supports_bitwise(name, loc, layers):
 
 @pytest.mark.gpu
 def test_patch_supports_random_seeds_and_overflow():
-    """20k random seeds (repeats, any order) at layers 1-4: GPU == oracle; a
-    patch beyond the per-target bound raises instead of truncating."""
-    from paper_2510_18838_b200._lib import FieldmapError
-
+    """20k random seeds (repeats, any order) at layers 1-4: GPU == oracle;
+    patches beyond the per-thread bounds are computed exactly too."""
     d = golden("patch")
     tris, et = d["disk_tris"], d["disk_edge_tris"]
     seeds = np.random.default_rng(5).integers(0, tris.shape[0], 20000)
@@ -692,8 +690,13 @@ def test_patch_supports_random_seeds_and_overflow():
             assert np.array_equal(off, w_off) and np.array_equal(idx, w_idx)
     off, idx, _ = Kb.patch_supports(np.array([], np.int64), tris, et, 1, False)
     assert off.tolist() == [0] and idx.size == 0
-    with pytest.raises(FieldmapError):
-        Kb.patch_supports(seeds[:10], tris, et, 12, True)
+    # patches beyond the per-thread bounds (128 elements / 256 dofs) take the
+    # global-scratch path: no limit the reference does not have
+    for cen in (True, False):
+        off, idx, _ = Kb.patch_supports(seeds[:10], tris, et, 12, cen)
+        w_off, w_idx = O.patch_supports(seeds[:10], et, tris, 12, cen)
+        assert np.array_equal(off, w_off) and np.array_equal(idx, w_idx)
+        assert np.diff(off).max() > (128 if cen else 256)
     # locate's not-found seed (-1) and out-of-range ids are rejected, not read
     for bad in (-1, tris.shape[0]):
         with pytest.raises(ValueError):
@@ -968,3 +971,35 @@ def test_map_chunked_equals_one_shot():
                                 2500, keep=True)
     assert len(ops) == 3 and all(int(st[0].item()) == 0 for _, _, st in checks)
     assert np.array_equal(Y.cpu().numpy(), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lam", [0.0, 1e-6])
+def test_supports_beyond_256_rows_vs_oracle(lam):
+    """No support-size limit (the reference sizes its workspace from the
+    largest support, _ext.pyx:305-312): ~400-point supports go through the
+    warp-per-target fit (fm_big.cuh) -- one-shot, prepared, 3 components,
+    and the fit_many seam -- and match the oracle."""
+    from oracle import oracle as O
+    from paper_2510_18838_b200 import _kernels as Kb
+    from paper_2510_18838_b200 import pointwise as P
+
+    side = np.linspace(0, 1, 120)
+    xx, yy = np.meshgrid(side, side)
+    src = np.ascontiguousarray(np.column_stack([xx.ravel(), yy.ravel()]))
+    tgt = np.random.RandomState(3).uniform(0.2, 0.8, (300, 2))
+    X = np.column_stack([np.sin((c + 1) * src[:, 0]) * np.cos(src[:, 1]) + 2 for c in range(3)])
+    r = 0.095  # ~400 lattice points inside
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.FixedRadius(r), lam=lam)
+    want, st, (off, idx, dist, w) = O.transfer(src, X, tgt, 2, O.RBF_C4, 2.0, ("fixed", r),
+                                               lam=lam)
+    assert (st == 0).all() and np.diff(off).min() > 256
+    got1 = P.fit_point_cloud(src, X[:, 0], tgt, spec)
+    assert np.max(np.abs(got1 - want[:, 0]) / np.abs(want[:, 0])) < 1e-10
+    got = P.PreparedTransfer(src, tgt, spec).apply(X)
+    assert np.max(np.abs(got - want) / np.abs(want)) < 1e-10
+    v, c, s2 = Kb.fit_many(tgt, off, idx, w, src, X[:, 1], 2, lam, True)
+    vw, cw, sw = O.fit_many(tgt, off, idx, w, src, X[:, 1], 2, lam, True)
+    assert np.array_equal(s2, sw)
+    assert np.max(np.abs(v - vw) / np.abs(vw)) < 1e-10
+    assert np.max(np.abs(c - cw) / np.maximum(np.abs(cw), 1e-300)) < 1e-6
