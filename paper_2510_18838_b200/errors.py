@@ -36,3 +36,11 @@ class ExtrinsicEvaluationError(FieldBridgeError):
     def __init__(self, message, batch=None):
         super().__init__(message)
         self.batch = batch
+
+
+class PartitionError(FieldBridgeError):
+    """Invalid partition request (errors.py:51)."""
+
+
+class ExchangeError(FieldBridgeError):
+    """Routing plan and payload disagree (errors.py:55)."""

@@ -330,7 +330,38 @@ def cycle_cases():
     save("cycle", **out)
 
 
+def rendezvous_cases():
+    """coupled_transfer's pointwise branch (rendezvous.py:452-495, 601-629):
+    two square meshes partitioned by rcb, a rendezvous grid, the coupled
+    field and the MessageStats table, for several rank counts."""
+    from fieldbridge.rendezvous import build_rdv_partition, coupled_transfer, rcb_partition
+    from fieldbridge.pointwise import FitSpec, FixedRadius, RadialBasisSpec, RbfKind
+
+    ma, mb = fb.square(30), fb.square(22)
+    f = np.sin(ma.coords[:, 0]) * np.cos(ma.coords[:, 1]) + 2
+    field = fb.Field(ma, "vertices", 1, f)
+    lo = np.minimum(ma.bbox[0], mb.bbox[0])
+    hi = np.maximum(ma.bbox[1], mb.bbox[1])
+    r_c = 2.0 * ma.mean_edge_length
+    spec = FitSpec(2, RadialBasisSpec(RbfKind.C4, a=2.0), FixedRadius(r_c))
+    out = {"coords_a": ma.coords, "values_a": f, "coords_b": mb.coords, "lo": lo, "hi": hi,
+           "r_c": r_c}
+    for na, nb, nr, grid in ((4, 2, 3, (6, 5)), (2, 4, 4, (7, 7)), (1, 1, 1, (3, 3))):
+        rdv = build_rdv_partition((lo, hi), grid[0], grid[1], nr)
+        pa, pb = rcb_partition(ma, na), rcb_partition(mb, nb)
+        res, stats = coupled_transfer(field, pa, mb, pb, rdv, spec)
+        key = f"{na}_{nb}_{nr}"
+        out[f"own_a_{key}"] = pa.dof_owner("vertices")
+        out[f"own_b_{key}"] = pb.dof_owner("vertices")
+        out[f"grid_{key}"] = np.array(grid)
+        out[f"values_{key}"] = res.values
+        out[f"stats_{key}"] = np.array([row[2:] for row in stats.table()], dtype=np.int64)
+        out[f"stats_roles_{key}"] = np.array([f"{row[0]}:{row[1]}" for row in stats.table()])
+    save("rendezvous", **out)
+
+
 if __name__ == "__main__":
+    rendezvous_cases()
     cycle_cases()
     patch_cases()
     locate_cases()
