@@ -30,9 +30,10 @@ def launch_totals(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, mi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    ni = h.index("Metric Name") if "Metric Name" in h else None
     tot = OrderedDict()
     for r in rows[hi + 1:]:
-        if len(r) <= mi:
+        if len(r) <= mi or (ni is not None and r[ni] != "gpu__time_duration.sum"):
             continue
         v = float(r[mi].replace(",", ""))
         scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0,
@@ -74,33 +75,17 @@ def raw(rep):
     return res
 
 
-def hot_lines(rep, kernel, n=12):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
-                          "cuda,sass", "-k", "regex:" + kernel], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    cur, hdr, agg = None, None, []
-    for r in rows:
-        if not r:
-            continue
-        if r[0] == "File Path":
-            cur = r[1].split("/")[-1]
-            continue
-        if r[0] == "Line No":
-            hdr = r
-            continue
-        if hdr and r[0].isdigit():
-            d = dict(zip(hdr, r))
-            try:
-                agg.append((cur, int(r[0]), r[1].strip()[:80],
-                            int(d.get("Warp Stall Sampling (All Samples)") or 0),
-                            int(d.get("Instructions Executed") or 0)))
-            except ValueError:
-                pass
-    ts = sum(a[3] for a in agg) or 1
-    ti = sum(a[4] for a in agg) or 1
+def hot_lines(rep, kernel, n=12, launch=None):
+    """Hottest source lines (by stall samples) of ONE launch of `kernel` (the
+    launch-th matching launch: one size-bucket instantiation at a time)."""
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from ncu_lines import lines
+
+    agg = lines(rep, kernel, launch)
+    ts = sum(a[1] for a in agg.values()) or 1
+    ti = sum(a[2] for a in agg.values()) or 1
     return [(f, ln, src, 100.0 * s / ts, 100.0 * i / ti)
-            for f, ln, src, s, i in sorted(agg, key=lambda a: -a[3])[:n]]
+            for (f, ln), (src, s, i, _t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:n]]
 
 
 def main():
@@ -131,7 +116,9 @@ def main():
             for m, v in rw.get(k, {}).items():
                 lines.append(f"- {m}: {v}")
             short = k.split("<")[0].split("::")[-1].replace("void ", "").strip()
-            hl = hot_lines(rep, short)
+            same = [x for x in det if x.split("<")[0].split("::")[-1].replace(
+                "void ", "").strip() == short]
+            hl = hot_lines(rep, short, launch=same.index(k))
             if hl:
                 lines += ["", "| file:line | stall samples | instructions | source |",
                           "|---|---|---|---|"]
