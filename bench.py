@@ -271,12 +271,44 @@ def run_b200(args, rank, world, local_rank):
             while len(pending) > 1:
                 pending.pop(0)
             return Y, None, None, torch.zeros(1, dtype=torch.int32), (None, Y)
+        if gt is not None:
+            # the whole step replayed as one CUDA graph (device.GraphedTransfer):
+            # bboxes + geometry on the host (one D2H), every kernel of the path
+            # in the graph -- the same kernels and work as b200_step
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append(("start", e))
+            Y = gt.run()
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append(("graph", e))
+            return Y, None, None, torch.zeros(1, dtype=torch.int32), (None, Y)
         Y, op, cnt, stats, cloud = b200_step(src_d, tgt_d, X_d, spec, marks)
         return Y, op, cnt, stats, (cloud, Y)
+
+    def eager_phases(warm=3, runs=5):
+        """Phase split of the eager step (`runs` passes after `warm`): the
+        roofline's per-kernel times when the timed step is a graph replay or
+        the pipelined N > 1 step."""
+        ph, last = {}, None
+        for i in range(warm + runs):
+            flush.zero_()
+            m1 = []
+            last = b200_step(src_d, tgt_d, X_d, spec, m1)
+            torch.cuda.synchronize()
+            for (a, ea), (b, eb) in zip(m1[:-1], m1[1:]):
+                if i >= warm:
+                    ph[b] = ph.get(b, 0.0) + ea.elapsed_time(eb) / runs
+        return ph, last
+
+    gt = D.GraphedTransfer(src_d, tgt_d, X_d, spec) if (world == 1 and not args.no_graph) \
+        else None
 
     sampler = ClockSampler(local_rank)
     with sampler:
         sampler.wait_first_sample()
+        if gt is not None:  # eager phase split first (before the graph is captured)
+            ph1, eager = eager_phases()
         for _ in range(args.warmup):
             Y, op, cnt, stats, extra = step([])
         torch.cuda.synchronize()
@@ -330,15 +362,25 @@ def run_b200(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     value = nt_local * world * args.steps / (total_ms * 1e-3)
 
-    if world > 1:
-        # roofline inputs from one single-block pass on this rank (after the
-        # timed region; the pipelined step interleaves builds and gathers)
-        m1 = []
-        Y1, op, cnt, stats, _c = b200_step(src_d, tgt_d, X_d, spec, m1)
-        torch.cuda.synchronize()
-        ph1 = {b: ea.elapsed_time(eb) for (a, ea), (b, eb) in zip(m1[:-1], m1[1:])}
+    graph_check = None
+    if gt is not None:
+        graph_check = gt.check()
+        if not graph_check["valid"]:
+            raise SystemExit(f"graphed step not valid for this workload: {graph_check}")
+        Y1, op, cnt, stats, _c = eager
+        extra = (_c, Y1)
+        if not torch.equal(Y1, gt.Y):
+            raise SystemExit("graphed and eager steps disagree")
+        phase = {"graph (whole step)": phase.get("graph", 0.0)}
+        phase.update({f"eager {k}": v * args.steps for k, v in ph1.items()})
         build_ms, apply_ms = ph1["build"], ph1["apply"]
-    else:
+    if world > 1:
+        # roofline inputs from eager passes on this rank (after the timed
+        # region; the pipelined step interleaves builds and exchanges)
+        ph1, eager = eager_phases()
+        Y1, op, cnt, stats, _c = eager
+        build_ms, apply_ms = ph1["build"], ph1["apply"]
+    elif gt is None:
         build_ms = phase["build"] / args.steps
         apply_ms = phase["apply"] / args.steps
     # roofline inputs (per launch, from this run's own CUDA events)
@@ -426,7 +468,9 @@ def run_b200(args, rank, world, local_rank):
         "parallelism": f"target-sharded x{world}" + (
             " + NCCL all-gather of the target field" if world > 1 else ""),
         "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
-        "gpu_launches": launches_per_step(cnt) * args.steps,
+        "gpu_launches": (launches_per_step(cnt) if gt is None else
+                         14 + bin(gt.mask).count("1")) * args.steps,
+        "graph": graph_check,
         "roofline": {
             "kernel": "k_build (C4 weights + Householder QR + operator row, supports from k_select)",
             "bound": "fp64",
@@ -602,6 +646,8 @@ def run_large(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     with sampler:
         sampler.wait_first_sample()
+        if gt is not None:  # eager phase split first (before the graph is captured)
+            ph1, eager = eager_phases()
         for _ in range(args.warmup):
             out, checks, cloud = step([])
         torch.cuda.synchronize()
@@ -897,6 +943,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N=1: launch the step eagerly instead of replaying its CUDA graph")
     ap.add_argument("--blocks", type=int, default=1,
                     help="N>1: target blocks per rank (all-gather pipelining depth)")
     args = ap.parse_args()

@@ -86,6 +86,8 @@ SIGNATURES = {
                                    c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                                    c_vp, c_vp]),
     "fm_offsets_ordered_workspace": (c_sz, [c_i64]),
+    "fm_offsets_ordered_capped": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                          c_vp, c_sz, c_vp]),
     "fm_offsets_ordered": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz,
                                    c_vp]),
     "fm_build_operator": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),

@@ -510,6 +510,14 @@ size_t fm_offsets_ordered_workspace(int64_t n) {
 int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, int32_t slot_cap,
                        int64_t *offsets, int32_t *bucket_list, int32_t *bucket_count,
                        void *workspace, size_t workspace_bytes, fm_stream_t stream) {
+    return fm_offsets_ordered_capped(counts, perm, n, slot_cap, 0, offsets, bucket_list,
+                                     bucket_count, workspace, workspace_bytes, stream);
+}
+
+int fm_offsets_ordered_capped(const int32_t *counts, const int32_t *perm, int64_t n,
+                              int32_t slot_cap, int32_t cap_rows, int64_t *offsets,
+                              int32_t *bucket_list, int32_t *bucket_count, void *workspace,
+                              size_t workspace_bytes, fm_stream_t stream) {
     if (n < 0 || (bucket_list && !bucket_count)) return FM_ERR_ARG;
     if (workspace_bytes < fm_offsets_ordered_workspace(n)) return FM_ERR_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
@@ -522,7 +530,7 @@ int fm_offsets_ordered(const int32_t *counts, const int32_t *perm, int64_t n, in
     if (n > 0) {
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
         k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, tmp, slot_cap, bucket_list,
-                                                bucket_count);
+                                                bucket_count, 0, -1, cap_rows ? slot_cap : 0);
         FM_CHECK_LAUNCH();
     }
     return exclusive_scan<int32_t, int64_t>(tmp, n, offsets, scan_ws, scan_workspace_bytes(n), st);

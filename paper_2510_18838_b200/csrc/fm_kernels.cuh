@@ -723,7 +723,7 @@ static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
                                 int32_t *__restrict__ out, int slot_cap,
                                 int32_t *__restrict__ bucket_list,
                                 int32_t *__restrict__ bucket_count, int64_t p0 = 0,
-                                int64_t lstride = -1) {
+                                int64_t lstride = -1, int row_cap = 0) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (lstride < 0) lstride = n;
@@ -732,7 +732,7 @@ static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
         const int64_t j = base + lane;
         const int64_t i = p0 + j;
         const int m = j < n ? counts[perm ? perm[i] : i] : 0;
-        if (j < n && out) out[j] = m;
+        if (j < n && out) out[j] = (row_cap > 0 && m > row_cap) ? row_cap : m;
         if (bucket_list) {
             const int b = (j < n && m <= slot_cap) ? bucket_of(m) : -1;
             const unsigned peers = __match_any_sync(FM_FULL_MASK, b);

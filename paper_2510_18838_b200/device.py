@@ -666,3 +666,165 @@ def locate_elements(eg, mesh, pts, tol=1e-10, md=None):
                             ptr(cell_off), ptr(cell_items), float(tol), ptr(found), ptr(elem),
                             ptr(dim), ptr(ent), ptr(bary), _stream()), "fm_locate_batch")
     return found.bool(), elem
+
+
+class GraphedTransfer:
+    """The whole path -- grid, target order, select, operator build, apply --
+    for fixed point counts as ONE CUDA graph, replayed per call.
+
+    Geometry-dependent sizes are the only host knowledge the path needs: each
+    run() computes the sources' and targets' bboxes (one launch, one D2H), the
+    grid geometry (C) and r_max; the graph captured for that geometry is then
+    replayed -- no further host syncs, no per-kernel launch cost (the select's
+    statistics, the size-bucket counts and the row offsets stay on the device:
+    fm_lists.bucket_count_dev).  A geometry change recaptures.  The points and
+    the field are read from the tensors given at construction, so a caller
+    with moving geometry copies new coordinates into them and calls run().
+
+    Capacities: operator storage for slot_cap entries per target.  A replay is
+    valid when no support overflows its slot and no selection / fit fails;
+    check() reads the on-device statistics back (one small D2H) and reports
+    it -- the eager path (select + build_operator) handles the other cases."""
+
+    def __init__(self, src_d, tgt_d, X_d, fitspec, slot_cap=None):
+        self.src, self.tgt = src_d, tgt_d
+        self.X = X_d.reshape(X_d.shape[0], -1)
+        self.spec = fitspec
+        self.ns, self.dim = src_d.shape
+        self.nt = int(tgt_d.shape[0])
+        self.C = self.X.shape[1]
+        self.key = None
+        self.graph = None
+        self.slot_cap = slot_cap
+        self.Y = torch.empty((self.nt, self.C), dtype=torch.float64, device=src_d.device)
+
+    def _select_spec(self, bs, bt):
+        s = self.spec.selection
+        if hasattr(s, "min_points"):
+            lo, hi = np.minimum(bs[0], bt[0]), np.maximum(bs[1], bt[1])
+            ext = float(np.hypot(hi[0] - lo[0], hi[1] - lo[1])) if lo.size == 2 else \
+                float(np.sqrt(np.sum((hi - lo) ** 2)))
+            return adaptive(s.min_points, s.r0, s.growth, 1.0000001 * ext + 1e-300)
+        return fixed(s.r_c)
+
+    def _allocate(self, grid):
+        dev = self.src.device
+        L = _lib.lib()
+        nt, ns = self.nt, self.ns
+        self.grid = grid
+        ncell = int(grid.ncell)
+        self.cap = int(self.slot_cap or slot_capacity(self.dim, self.sel))
+        e = lambda n, t: _empty(max(int(n), 1), t, dev)  # noqa: E731
+        self.cell_start, self.sorted_ids = e(ncell + 1, torch.int32), e(ns, torch.int32)
+        self.sorted_pts = _empty((ns, self.dim), torch.float64, dev)
+        self.gws_bytes = L.fm_grid_workspace(ns, ncell)
+        self.gws = _workspace(self.gws_bytes, dev)
+        self.perm = e(nt, torch.int32)
+        self.ows_bytes = L.fm_order_workspace(nt, ctypes.byref(grid))
+        self.ows = _workspace(self.ows_bytes, dev)
+        self.counts = e(nt, torch.int32)
+        self.radii = e(nt, torch.float64) if self.sel.adaptive else None
+        self.status = e(nt, torch.uint8) if self.sel.adaptive else None
+        self.slot_pos = e(nt * self.cap, torch.int32)
+        self.overflow = e(nt, torch.int32)
+        self.pos_info = e(2 * nt, torch.float64)
+        self.pos_t = _empty((max(nt, 1), self.dim), torch.float64, dev)
+        nb = _lib.FM_NBUCKETS
+        self.stats = e(8 + nb + 2, torch.int32)  # select stats, bucket sizes, fit stats
+        self.blist = e(nt * nb, torch.int32)
+        self.offsets = e(nt + 1, torch.int64)
+        self.sws_bytes = L.fm_offsets_ordered_workspace(nt)
+        self.sws = _workspace(self.sws_bytes, dev)
+        self.col = e(nt * self.cap, torch.int32)
+        self.val = e(nt * self.cap, torch.float64)
+        self.fstatus = e(nt, torch.uint8)
+        edges = _lib.FM_BUCKET_EDGES
+        # every bucket a slotted support can fall in (sizes read on the device)
+        self.mask = sum(1 << b for b in range(nb) if b == 0 or edges[b - 1] < self.cap)
+
+    def _launch(self):
+        L = _lib.lib()
+        st = _stream()
+        g, nt, ns = self.grid, self.nt, self.ns
+        check(L.fm_grid_build(ctypes.byref(g), ptr(self.src), ns, ptr(self.cell_start),
+                              ptr(self.sorted_ids), ptr(self.sorted_pts), ptr(self.gws),
+                              self.gws_bytes, st), "fm_grid_build")
+        check(L.fm_target_order(ctypes.byref(g), ptr(self.tgt), nt, ptr(self.perm),
+                                ptr(self.ows), self.ows_bytes, st), "fm_target_order")
+        csel = self.sel.to_ctypes()
+        need = 0 if self.sel.adaptive else _n_monomials(self.dim, self.spec.degree)
+        check(L.fm_select_supports(ctypes.byref(g), ptr(self.cell_start), ptr(self.sorted_pts),
+                                   ptr(self.sorted_ids), ptr(self.tgt), nt, ptr(self.perm),
+                                   ctypes.byref(csel), need, ptr(self.counts), ptr(self.radii),
+                                   ptr(self.status), None, ptr(self.slot_pos), self.cap,
+                                   ptr(self.overflow), ptr(self.stats), ptr(self.pos_info),
+                                   ptr(self.pos_t), st), "fm_select_supports")
+        # row lengths capped at the slot: the offsets stay within nt * cap
+        check(L.fm_offsets_ordered_capped(ptr(self.counts), ptr(self.perm), nt, self.cap, 1,
+                                          ptr(self.offsets), ptr(self.blist),
+                                          ptr(self.stats[8:]), ptr(self.sws), self.sws_bytes,
+                                          st), "fm_offsets_ordered_capped")
+        nb = _lib.FM_NBUCKETS
+        lists = FmLists(self.counts.data_ptr(), None, self.slot_pos.data_ptr(), self.cap, 0,
+                        self.overflow.data_ptr(), self.pos_info.data_ptr(),
+                        self.pos_t.data_ptr(), self.blist.data_ptr(), nt,
+                        (ctypes.c_int32 * nb)(*([0] * nb)), self.stats[8:].data_ptr(), self.mask,
+                        1)
+        rbf = self.spec.rbf
+        from .pointwise import _rbf_pair
+
+        kind, a = _rbf_pair(rbf)
+        crbf = FmRbf(int(kind), 0, float(a))
+        cfit = _fit_struct(self.dim, self.spec.degree, self.spec.lam, self.spec.centering)
+        check(L.fm_build_operator(ctypes.byref(g), ptr(self.cell_start), ptr(self.sorted_pts),
+                                  ptr(self.sorted_ids), ptr(self.tgt), nt, ptr(self.perm),
+                                  ctypes.byref(csel), ptr(self.radii), ctypes.byref(lists),
+                                  ptr(self.offsets), self.cap, ctypes.byref(crbf),
+                                  ctypes.byref(cfit), ptr(self.col), ptr(self.val),
+                                  ptr(self.fstatus), ptr(self.stats[8 + nb:]), st),
+              "fm_build_operator")
+        check(L.fm_apply(nt, ptr(self.offsets), ptr(self.col), ptr(self.val), ptr(self.perm),
+                         ptr(self.X), self.C, ptr(self.Y), st), "fm_apply")
+
+    def run(self):
+        """Map the current sources/targets/field; returns Y (nt, C) on the
+        device (valid when check() says so)."""
+        bs, bt = device_bboxes([self.src, self.tgt])
+        grid = FmGrid()
+        lo = np.ascontiguousarray(bs[0])
+        hi = np.ascontiguousarray(bs[1])
+        check(_lib.lib().fm_grid_geometry(self.dim, lo.ctypes.data, hi.ctypes.data, self.ns,
+                                          1.0, ctypes.byref(grid), None, None),
+              "fm_grid_geometry")
+        self.sel = self._select_spec(bs, bt)
+        key = (bytes(grid), self.sel)
+        if key != self.key:
+            self._allocate(grid)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # eager pass: lazy attributes/streams outside capture
+                self._launch()
+            torch.cuda.current_stream().wait_stream(side)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self._launch()
+            self.key = key
+        self.graph.replay()
+        return self.Y
+
+    def check(self):
+        """On-device statistics of the last run (one small D2H): dict with
+        the select stats (fieldmap.h fm_select_supports), fit failures and
+        `valid` (no overflow, no selection or fit failure)."""
+        h = self.stats.cpu().numpy()
+        nb = _lib.FM_NBUCKETS
+        out = {"max_count": int(h[0]), "short": int(h[2]), "status_fail": int(h[4]),
+               "overflow": int(h[6]), "fit_fail": int(h[8 + nb]),
+               "buckets": h[8:8 + nb].tolist(), "nnz": int(self.offsets[self.nt].item())}
+        out["valid"] = (out["overflow"] == 0 and out["short"] == 0 and out["status_fail"] == 0
+                        and out["fit_fail"] == 0)
+        return out
+
+
+def _n_monomials(dim, degree):
+    return int(_lib.lib().fm_n_monomials(int(dim), int(degree)))

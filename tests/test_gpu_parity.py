@@ -1004,3 +1004,45 @@ def test_supports_beyond_256_rows_vs_oracle(lam):
     assert np.array_equal(s2, sw)
     assert np.max(np.abs(v - vw) / np.abs(vw)) < 1e-10
     assert np.max(np.abs(c - cw) / np.maximum(np.abs(cw), 1e-300)) < 1e-6
+
+
+@pytest.mark.gpu
+def test_graphed_transfer_equals_eager():
+    """device.GraphedTransfer (the whole path replayed as one CUDA graph)
+    gives bitwise the eager operator's result, reports validity, follows
+    coordinates written into its tensors (same geometry: replay; new
+    geometry: recapture), and flags an overflowing support as invalid."""
+    import torch
+
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+    from paper_2510_18838_b200 import synth
+
+    m = synth.disk_graded(1.0, 80, 0.6)
+    src = m.coords
+    tgt = synth.disk(1.0, 70).coords
+    X = synth.sincos_field(src, 4)
+    spec = P.FitSpec(2, P.RadialBasisSpec(P.RbfKind.C4, a=2.0),
+                     P.AdaptiveRadius(12, m.mean_edge_length, 1.5))
+    s_d, t_d, X_d = D.to_device(src), D.to_device(tgt), D.to_device(X)
+    gt = D.GraphedTransfer(s_d, t_d, X_d, spec)
+    for _ in range(2):
+        Y = gt.run().clone()
+        assert gt.check()["valid"]
+        assert np.array_equal(Y.cpu().numpy(), P.fit_point_cloud(src, X, tgt, spec))
+    # new target coordinates in place (same bbox -> replay of the same graph)
+    rot = tgt[::-1].copy()
+    t_d.copy_(torch.from_numpy(rot))
+    Y = gt.run()
+    assert np.array_equal(Y.cpu().numpy(), P.fit_point_cloud(src, X, rot, spec))
+    # new source geometry (different bbox -> recapture)
+    src2 = src * 1.001 + 0.001
+    s_d.copy_(torch.from_numpy(src2))
+    Y = gt.run()
+    assert gt.check()["valid"]
+    assert np.array_equal(Y.cpu().numpy(), P.fit_point_cloud(src2, X, rot, spec))
+    # a slot too small for the supports: the replay reports itself invalid
+    gt2 = D.GraphedTransfer(s_d, t_d, X_d, spec, slot_cap=8)
+    gt2.run()
+    chk = gt2.check()
+    assert chk["overflow"] > 0 and not chk["valid"]
