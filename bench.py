@@ -248,7 +248,7 @@ def run_b200(args, rank, world, local_rank):
 
     from paper_2510_18838_b200 import device as D
     from paper_2510_18838_b200 import pointwise as P
-    from paper_2510_18838_b200.distributed import map_gathered
+    from paper_2510_18838_b200.distributed import map_gathered  # noqa: F401
 
     torch.cuda.set_device(local_rank)
     src, tgt, X, spec, desc = workload(args.config, rank)
@@ -265,8 +265,17 @@ def run_b200(args, rank, world, local_rank):
             # the exchange of this step completing under the next step
             # (distributed.map_gathered pipelined); the timed region ends
             # after the last exchange has completed
-            Y, done = map_gathered(src_d, tgt_d, X_d, spec, nblocks=args.blocks, marks=marks,
-                                   pipelined=True)
+            if gg is not None:  # the rank's compute as a CUDA graph, then the pushes
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append(("start", e))
+                Y, done = gg.step()
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append(("graph+push", e))
+            else:
+                Y, done = map_gathered(src_d, tgt_d, X_d, spec, nblocks=args.blocks,
+                                       marks=marks, pipelined=True)
             pending.append(done)
             while len(pending) > 1:
                 pending.pop(0)
@@ -303,6 +312,11 @@ def run_b200(args, rank, world, local_rank):
 
     gt = D.GraphedTransfer(src_d, tgt_d, X_d, spec) if (world == 1 and not args.no_graph) \
         else None
+    gg = None
+    if world > 1 and not args.no_graph:
+        from paper_2510_18838_b200.distributed import GraphedGather
+
+        gg = GraphedGather(src_d, tgt_d, X_d, spec)
 
     sampler = ClockSampler(local_rank)
     with sampler:
@@ -363,6 +377,10 @@ def run_b200(args, rank, world, local_rank):
     value = nt_local * world * args.steps / (total_ms * 1e-3)
 
     graph_check = None
+    if gg is not None:
+        graph_check = gg.check()
+        if not all(c["valid"] for c in graph_check):
+            raise SystemExit(f"graphed step not valid for this workload: {graph_check}")
     if gt is not None:
         graph_check = gt.check()
         if not graph_check["valid"]:

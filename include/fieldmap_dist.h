@@ -56,6 +56,13 @@ int fm_build_apply_blocks(const fm_grid *grid, const int32_t *cell_start,
                           int32_t npeers, void *const *peer_Y, fm_stream_t stream,
                           fm_stream_t comm);
 
+/* Push `bytes` at device `src` (this GPU) to offset dst_offset of every
+ * peer buffer peer_bases[q] (IPC pointers): one copy-engine transfer per peer
+ * on its own stream, after the work already queued on `stream`; `comm` waits
+ * for all of them (close the exchange with a collective on `comm`). */
+int fm_push_rows(const void *src, size_t bytes, size_t dst_offset, int32_t npeers,
+                 void *const *peer_bases, fm_stream_t stream, fm_stream_t comm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -105,6 +105,7 @@ SIGNATURES = {
     "fm_ipc_export": (c_i32, [c_vp, c_vp]),
     "fm_ipc_open": (c_i32, [c_vp, P(c_vp)]),
     "fm_ipc_close": (c_i32, [c_vp]),
+    "fm_push_rows": (c_i32, [c_vp, c_sz, c_sz, c_i32, c_vp, c_vp, c_vp]),
     "fm_build_apply_blocks": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
                                       c_vp, P(FmLists), c_vp, c_i32, P(FmRbf), P(FmFit), c_vp,
                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp,

@@ -149,4 +149,30 @@ int fm_build_apply_blocks(const fm_grid *grid, const int32_t *cell_start,
     return rc;
 }
 
+int fm_push_rows(const void *src, size_t bytes, size_t dst_offset, int32_t npeers,
+                 void *const *peer_bases, fm_stream_t stream, fm_stream_t comm) {
+    if (npeers < 0 || npeers > FM_MAX_PEERS || (npeers > 0 && (!src || !peer_bases || !comm)))
+        return FM_ERR_ARG;
+    if (npeers == 0 || bytes == 0) return FM_OK;
+    cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)comm;
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return FM_ERR_CUDA;
+    cudaEventRecord(ev, st);
+    PeerStreams *ps = peer_streams(npeers);
+    int rc = FM_OK;
+    for (int q = 0; q < npeers && rc == FM_OK; q++) {
+        cudaStream_t sq = ps ? ps->s[q] : cs;
+        cudaStreamWaitEvent(sq, ev, 0);
+        char *dst = reinterpret_cast<char *>(peer_bases[q]) + dst_offset;
+        if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, sq) != cudaSuccess)
+            rc = FM_ERR_CUDA;
+        if (ps) {
+            cudaEventRecord(ps->join[q], sq);
+            cudaStreamWaitEvent(cs, ps->join[q], 0);
+        }
+    }
+    cudaEventDestroy(ev);
+    return rc;
+}
+
 }  // extern "C"

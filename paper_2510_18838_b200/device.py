@@ -686,7 +686,7 @@ class GraphedTransfer:
     check() reads the on-device statistics back (one small D2H) and reports
     it -- the eager path (select + build_operator) handles the other cases."""
 
-    def __init__(self, src_d, tgt_d, X_d, fitspec, slot_cap=None):
+    def __init__(self, src_d, tgt_d, X_d, fitspec, slot_cap=None, out=None):
         self.src, self.tgt = src_d, tgt_d
         self.X = X_d.reshape(X_d.shape[0], -1)
         self.spec = fitspec
@@ -696,7 +696,10 @@ class GraphedTransfer:
         self.key = None
         self.graph = None
         self.slot_cap = slot_cap
-        self.Y = torch.empty((self.nt, self.C), dtype=torch.float64, device=src_d.device)
+        self.Y = out if out is not None else torch.empty((self.nt, self.C), dtype=torch.float64,
+                                                          device=src_d.device)
+        if tuple(self.Y.shape) != (self.nt, self.C) or not self.Y.is_contiguous():
+            raise ValueError("out must be a contiguous (nt, C) tensor")
 
     def _select_spec(self, bs, bt):
         s = self.spec.selection

@@ -244,6 +244,55 @@ class _Done:
         return True
 
 
+class GraphedGather:
+    """map_gathered(pipelined=True) with the rank's compute replayed as a CUDA
+    graph (device.GraphedTransfer writing straight into this rank's slot of
+    the receive buffer): per step, the bbox/geometry check, the graph, then
+    the copy-engine pushes of the rank's rows to every peer and the closing
+    collective on the side stream.  Two receive buffers (and two graphs)
+    alternate, so a step's exchange completes under the next step."""
+
+    def __init__(self, src_d, tgt_d, X_d, fitspec, group=None):
+        from . import device as D
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.group = group
+        self.nt = int(tgt_d.shape[0])
+        self.C = X_d.reshape(X_d.shape[0], -1).shape[1]
+        self.ex = [_exchange(self.world, self.rank, self.nt, self.C, group, slot)
+                   for slot in (0, 1)]
+        self.gt = [D.GraphedTransfer(src_d, tgt_d, X_d, fitspec, out=e.full[self.rank])
+                   for e in self.ex]
+        self.slot = 0
+
+    def step(self):
+        """One mapping of the current points/field; returns (field, done)."""
+        slot = self.slot
+        self.slot ^= 1
+        ex, gt = self.ex[slot], self.gt[slot]
+        main = torch.cuda.current_stream()
+        comm = _comm_stream()
+        comm.wait_stream(main)
+        gt.run()
+        work = None
+        if self.world > 1:
+            nbytes = self.nt * self.C * 8
+            _check(_lib().fm_push_rows(ctypes.c_void_p(gt.Y.data_ptr()), nbytes,
+                                       self.rank * nbytes, len(ex.peers),
+                                       (ctypes.c_void_p * len(ex.peers))(*ex.peers),
+                                       ctypes.c_void_p(main.cuda_stream),
+                                       ctypes.c_void_p(comm.cuda_stream)), "fm_push_rows")
+            with torch.cuda.stream(comm):
+                flag = torch.zeros(1, dtype=torch.float32, device=gt.Y.device)
+                work = dist.all_reduce(flag, group=self.group, async_op=True)
+        out = ex.full.reshape(self.world * self.nt, self.C)
+        return out, (work if work is not None else _Done())
+
+    def check(self):
+        return [gt.check() for gt in self.gt if gt.key is not None]
+
+
 def _lib():
     from . import _lib as L
 
