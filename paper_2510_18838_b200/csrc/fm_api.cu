@@ -40,14 +40,17 @@ __global__ void k_scale_points(const double *__restrict__ pts, int64_t n, int di
 // (col, val) stream through shared memory with coalesced loads, then each
 // row group of L lanes (V consecutive components per lane, C = L*V) gathers
 // the X rows -- one 16-byte load per lane per nonzero, 8 in flight.
-constexpr int kApplyChunk = 256;  // staged nonzeros per warp and pass
-
+// CH = staged nonzeros per warp and pass (measured: 256 beats 128 / 64 / 32,
+// 0.150 vs 0.178 / 0.234 / 0.377 ms on C2 -- the per-pass overhead outweighs
+// the L1 left to cache X); CS = evict-first (col, val) loads (no gain).
+// A variant double-buffering the next tile's (col, val) with cp.async was
+// slower (0.166 ms): the kernel is bound by L1 wavefronts, not by latency.
 #ifdef FM_APPLY_MINB
 #define FM_APPLY_BOUNDS __launch_bounds__(256, FM_APPLY_MINB)
 #else
 #define FM_APPLY_BOUNDS __launch_bounds__(256)
 #endif
-template <int L, int V>
+template <int L, int V, int CH, bool CS>
 __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
                                                const int32_t *__restrict__ col,
                                                const double *__restrict__ val,
@@ -60,8 +63,8 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
 #define FM_APPLY_U 8
 #endif
     constexpr int U = FM_APPLY_U;
-    __shared__ int32_t s_col[8][kApplyChunk];
-    __shared__ double s_val[8][kApplyChunk];
+    __shared__ int32_t s_col[8][CH];
+    __shared__ double s_val[8][CH];
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int rr = lane / L, li = lane % L;
@@ -80,11 +83,11 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = 0.0;
-        for (int64_t cs = tb; cs < te; cs += kApplyChunk) {
-            const int n = (int)(te - cs < kApplyChunk ? te - cs : kApplyChunk);
+        for (int64_t cs = tb; cs < te; cs += CH) {
+            const int n = (int)(te - cs < CH ? te - cs : CH);
             for (int i = lane; i < n; i += 32) {
-                sc[i] = __ldg(col + cs + i);
-                sv[i] = __ldg(val + cs + i);
+                sc[i] = CS ? __ldcs(col + cs + i) : __ldg(col + cs + i);
+                sv[i] = CS ? __ldcs(val + cs + i) : __ldg(val + cs + i);
             }
             __syncwarp();
             const int j0 = (int)((rb > cs ? rb : cs) - cs);
@@ -147,7 +150,7 @@ __global__ void k_apply_generic(int64_t nrows, const int64_t *__restrict__ row_o
     }
 }
 
-template <int L, int V>
+template <int L, int V, int CH = 256, bool CS = false>
 static int launch_apply(int64_t nrows, const int64_t *row_off, const int32_t *col,
                         const double *val, const int32_t *row_target, const double *X, double *Y,
                         cudaStream_t st) {
@@ -156,7 +159,7 @@ static int launch_apply(int64_t nrows, const int64_t *row_off, const int32_t *co
     const int64_t tiles = (nrows + RPW - 1) / RPW;
     const int64_t need = (tiles + 7) / 8;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kSMs * 8));
-    k_apply<L, V><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
+    k_apply<L, V, CH, CS><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <math.h>
 #include <type_traits>
 #include <stdint.h>
@@ -17,6 +18,24 @@
             return FM_ERR_CUDA;                             \
         }                                                   \
     } while (0)
+
+// Debug builds (-DFM_DEBUG; scripts/build_variant.py debug -DFM_DEBUG) trap on
+// out-of-range indices at the path's gathers and scatters -- the bounds
+// checks standing in for compute-sanitizer, which this GPU pool does not run.
+#ifdef FM_DEBUG
+#define FM_DCHECK(cond)                                                                   \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("FM_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define FM_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 namespace fm {
 

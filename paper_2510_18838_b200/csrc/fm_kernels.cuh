@@ -256,6 +256,7 @@ __device__ __forceinline__ void build_core(const BuildArgs &b, const GroupSmem<G
     bool valid[ROWS];
     double w[ROWS], f[ROWS];
     const double inv_r = active ? 1.0 / r : 0.0;
+    FM_DCHECK(!active || (m >= 0 && m <= ROWS * G));
 #pragma unroll
     for (int q = 0; q < ROWS; q++) {
         const int i = q * G + glane;
@@ -375,6 +376,7 @@ __device__ __forceinline__ void stage_rows(const SearchArgs &s, const BuildArgs 
         const int i = q * G + glane;
         const bool v = fits && i < m;
         const int64_t sp = v ? S.spos[sl][i] : 0;
+        FM_DCHECK(sp >= 0 && (!v || i < b.slot_cap));
         if (DIM == 2)
             cp_async16(&S.pts[pb][i][0], s.sorted_pts + sp * DIM, v);
         else
@@ -645,6 +647,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
         bool slotted = false;
         if (active) {
             const int64_t tid = s.perm ? (int64_t)__ldg(s.perm + k) : k;
+            FM_DCHECK(tid >= 0 && tid < s.nt);
             double t[DIM];
             load_target<DIM>(s.targets, tid, true, t);
             double r;
@@ -686,6 +689,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
             const int64_t kr = tile * 32 + r;
             const int32_t *lp = lpos_all + (wbase + r) * stride;
             int32_t *op = slot_pos + kr * slot_cap;
+            FM_DCHECK(kr < s.nt && mr <= slot_cap);
             for (int e = lane; e < mr; e += 32) {
                 const int32_t p = lp[e] & kPosMask;
                 op[e] = p;

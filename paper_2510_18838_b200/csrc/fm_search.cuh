@@ -617,7 +617,10 @@ __device__ __forceinline__ int scan_thread(const GridDev &g, const int32_t *__re
             const int code = (d2 >= thr_mid ? 1 : 0) + (d2 >= thr_lo ? 1 : 0);
             nm += d2 < thr_mid;
             nl += d2 < thr_lo;
-            if (n < L.cap) L.e[n] = p | (code << kCodeShift);
+            if (n < L.cap) {
+                FM_DCHECK(p >= 0 && p <= kPosMask);
+                L.e[n] = p | (code << kCodeShift);
+            }
             n++;
         }
     };
@@ -650,8 +653,10 @@ __device__ __forceinline__ int scan_thread(const GridDev &g, const int32_t *__re
         const double hw = sqrt(fmax(hw2, 0.0) + eps_r2) * (1.0 + kSlackRel);
         const int64_t x0 = cell_of(t[0] - hw, g.lo[0], g.inv_d[0], g.n[0]);
         const int64_t x1 = cell_of(t[0] + hw, g.lo[0], g.inv_d[0], g.n[0]);
+        FM_DCHECK(x0 >= 0 && x1 < g.n[0] && base >= 0 && base + x1 + 1 <= st);
         const int32_t p0 = __ldg(cell_start + base + x0);
         const int32_t p1 = __ldg(cell_start + base + x1 + 1);
+        FM_DCHECK(0 <= p0 && p0 <= p1 && p1 <= __ldg(cell_start + st));
         int32_t p = p0;
         for (; p + 1 < p1; p += 2) {  // two point loads in flight
             double pa[DIM], pb[DIM];

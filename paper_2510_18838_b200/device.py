@@ -695,6 +695,7 @@ class GraphedTransfer:
         self.C = self.X.shape[1]
         self.key = None
         self.graph = None
+        self._fork = None
         self.slot_cap = slot_cap
         self.Y = out if out is not None else torch.empty((self.nt, self.C), dtype=torch.float64,
                                                           device=src_d.device)
@@ -749,11 +750,19 @@ class GraphedTransfer:
         L = _lib.lib()
         st = _stream()
         g, nt, ns = self.grid, self.nt, self.ns
+        # the target order needs only the grid geometry: it runs on a forked
+        # stream beside the source binning (a graph branch once captured)
+        main = torch.cuda.current_stream()
+        if self._fork is None:
+            self._fork = torch.cuda.Stream()
+        self._fork.wait_stream(main)
+        with torch.cuda.stream(self._fork):
+            check(L.fm_target_order(ctypes.byref(g), ptr(self.tgt), nt, ptr(self.perm),
+                                    ptr(self.ows), self.ows_bytes, _stream()), "fm_target_order")
         check(L.fm_grid_build(ctypes.byref(g), ptr(self.src), ns, ptr(self.cell_start),
                               ptr(self.sorted_ids), ptr(self.sorted_pts), ptr(self.gws),
                               self.gws_bytes, st), "fm_grid_build")
-        check(L.fm_target_order(ctypes.byref(g), ptr(self.tgt), nt, ptr(self.perm),
-                                ptr(self.ows), self.ows_bytes, st), "fm_target_order")
+        main.wait_stream(self._fork)
         csel = self.sel.to_ctypes()
         need = 0 if self.sel.adaptive else _n_monomials(self.dim, self.spec.degree)
         check(L.fm_select_supports(ctypes.byref(g), ptr(self.cell_start), ptr(self.sorted_pts),

@@ -53,6 +53,18 @@ def gather_target_field(Y_local, n_total, group=None):
     return out[:, 0] if squeeze else out
 
 
+def upload_replicated(host, group=None):
+    """Put a host array that every rank holds (the replicated source cloud or
+    source field) on every rank's GPU: each rank copies only its 1/world row
+    block over its own PCIe link (pinned host memory: asynchronous), and one
+    NCCL all-gather over NVLink assembles the whole array on every GPU.  The
+    ranks' PCIe links share the host's memory bandwidth, NVLink does not."""
+    world = dist.get_world_size(group)
+    lo, hi = shard_bounds(host.shape[0], dist.get_rank(group), world)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    return gather_target_field(host[lo:hi].to(dev, non_blocking=True), host.shape[0], group)
+
+
 class _RawCuda:
     """__cuda_array_interface__ view of library-allocated device memory."""
 

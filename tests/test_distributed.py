@@ -9,7 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_18838_b200.distributed import gather_target_field, shard_bounds, shard_sizes
+from paper_2510_18838_b200.distributed import (gather_target_field, shard_bounds, shard_sizes,
+                                               upload_replicated)
 
 
 def test_shard_bounds_cover_exactly():
@@ -38,7 +39,9 @@ def _worker(rank, world, port, n, C, q):
         lo, hi = shard_bounds(n, rank, world)
         got = gather_target_field(full[lo:hi].clone(), n)
         got1 = gather_target_field(full[lo:hi, 0].clone(), n)
-        q.put((rank, bool(torch.equal(got, full)), bool(torch.equal(got1, full[:, 0]))))
+        up = upload_replicated(full)  # every rank holds `full`; 1/world of it is copied
+        q.put((rank, bool(torch.equal(got, full) and torch.equal(up, full)),
+               bool(torch.equal(got1, full[:, 0]))))
     finally:
         dist.destroy_process_group()
 
