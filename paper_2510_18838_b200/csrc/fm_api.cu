@@ -531,7 +531,7 @@ int fm_offsets_ordered_capped(const int32_t *counts, const int32_t *perm, int64_
         cudaMemsetAsync(bucket_count, 0, sizeof(int32_t) * FM_NBUCKETS, st) != cudaSuccess)
         return FM_ERR_CUDA;
     if (n > 0) {
-        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
+        const int blocks = (int)std::min<int64_t>((n + 1023) / 1024, (int64_t)kSMs * 8);
         k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, tmp, slot_cap, bucket_list,
                                                 bucket_count, 0, -1, cap_rows ? slot_cap : 0);
         FM_CHECK_LAUNCH();
@@ -550,7 +550,7 @@ int fm_bucket_positions(const int32_t *counts, const int32_t *perm, int64_t p0, 
         return FM_ERR_CUDA;
     const int64_t n = p1 - p0;
     if (n > 0) {
-        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 16);
+        const int blocks = (int)std::min<int64_t>((n + 1023) / 1024, (int64_t)kSMs * 8);
         k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, n, nullptr, slot_cap, bucket_list,
                                                 bucket_count, p0, bucket_stride);
         FM_CHECK_LAUNCH();

@@ -718,37 +718,56 @@ __device__ __forceinline__ int bucket_of(int m) {
 }
 
 // counts in processing order (input of the ordered offsets scan) and,
-// with bucket_list, the positions partitioned by support size
-// (warp-aggregated appends: one atomic per bucket present in a warp)
+// with bucket_list, the positions partitioned by support size.  Appends are
+// aggregated per block: warps count into shared memory, then ONE global
+// atomic per bucket and block tile of 1024 positions reserves the block's
+// range (per-warp global atomics on the 9 bucket counters serialized).
 // positions p0 + [0, n): out (may be NULL) indexed from 0, bucket lists
 // with stride lstride holding absolute positions
-static __global__ void k_gather_counts(const int32_t *__restrict__ counts,
-                                const int32_t *__restrict__ perm, int64_t n,
-                                int32_t *__restrict__ out, int slot_cap,
-                                int32_t *__restrict__ bucket_list,
-                                int32_t *__restrict__ bucket_count, int64_t p0 = 0,
-                                int64_t lstride = -1, int row_cap = 0) {
+constexpr int kGatherItems = 4;
+static __global__ void __launch_bounds__(256) k_gather_counts(
+    const int32_t *__restrict__ counts, const int32_t *__restrict__ perm, int64_t n,
+    int32_t *__restrict__ out, int slot_cap, int32_t *__restrict__ bucket_list,
+    int32_t *__restrict__ bucket_count, int64_t p0 = 0, int64_t lstride = -1,
+    int row_cap = 0) {
+    __shared__ int s_cnt[FM_NBUCKETS];
+    __shared__ int s_base[FM_NBUCKETS];
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (lstride < 0) lstride = n;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
-         base += stride) {
-        const int64_t j = base + lane;
-        const int64_t i = p0 + j;
-        const int m = j < n ? counts[perm ? perm[i] : i] : 0;
-        if (j < n && out) out[j] = (row_cap > 0 && m > row_cap) ? row_cap : m;
-        if (bucket_list) {
-            const int b = (j < n && m <= slot_cap) ? bucket_of(m) : -1;
-            const unsigned peers = __match_any_sync(FM_FULL_MASK, b);
-            if (b >= 0) {
+    constexpr int kTile = 256 * kGatherItems;
+    for (int64_t base = (int64_t)blockIdx.x * kTile; base < n; base += (int64_t)gridDim.x * kTile) {
+        int b[kGatherItems], at[kGatherItems];
+        if (bucket_list && threadIdx.x < FM_NBUCKETS) s_cnt[threadIdx.x] = 0;
+        if (bucket_list) __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kGatherItems; it++) {
+            const int64_t j = base + it * 256 + threadIdx.x;
+            const int64_t i = p0 + j;
+            const int m = j < n ? __ldg(counts + (perm ? __ldg(perm + i) : i)) : 0;
+            if (j < n && out) out[j] = (row_cap > 0 && m > row_cap) ? row_cap : m;
+            b[it] = (j < n && m <= slot_cap) ? bucket_of(m) : -1;
+            at[it] = 0;
+            if (bucket_list) {
+                const unsigned peers = __match_any_sync(FM_FULL_MASK, b[it]);
                 const int leader = __ffs(peers) - 1;
-                int at = 0;
-                if (lane == leader) at = atomicAdd(bucket_count + b, __popc(peers));
-                at = __shfl_sync(peers, at, leader);
-                bucket_list[(int64_t)b * lstride + at + __popc(peers & ((1u << lane) - 1u))] =
-                    (int32_t)i;
+                int a0 = 0;
+                if (lane == leader && b[it] >= 0) a0 = atomicAdd(&s_cnt[b[it]], __popc(peers));
+                at[it] = __shfl_sync(FM_FULL_MASK, a0, leader) +
+                         __popc(peers & ((1u << lane) - 1u));
             }
         }
+        if (!bucket_list) continue;
+        __syncthreads();
+        if (threadIdx.x < FM_NBUCKETS) {
+            const int c = s_cnt[threadIdx.x];
+            s_base[threadIdx.x] = c ? atomicAdd(bucket_count + threadIdx.x, c) : 0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kGatherItems; it++)
+            if (b[it] >= 0)
+                bucket_list[(int64_t)b[it] * lstride + s_base[b[it]] + at[it]] =
+                    (int32_t)(p0 + base + it * 256 + threadIdx.x);
     }
 }
 

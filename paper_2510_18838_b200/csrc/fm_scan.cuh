@@ -15,8 +15,12 @@
 
 namespace fm {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+// Large tiles: a tile's look-back walks its predecessors 32 per round until
+// it meets an inclusive prefix, and the inclusive frontier advances ~32 tiles
+// per round, so the scan's critical path grows with the tile COUNT (2048-
+// element tiles: 489 tiles and ~14 us for 1M elements).
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 #define FM_SCAN_AGG (1ull << 62)
@@ -43,12 +47,27 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(
     const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
     long long v[kScanItems];
     long long local = 0;
+    // full tiles of a 16-byte aligned int32 input: 16-byte loads
+    const bool vec = sizeof(TIn) == 4 && (tile + 1) * kScanTile <= n &&
+                     ((uintptr_t)in & 15) == 0;
+    if (vec) {
 #pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        const int64_t i = base + k;
-        v[k] = i < n ? (long long)in[i] : 0;
-        local += v[k];
+        for (int k = 0; k < kScanItems; k += 4) {
+            const int4 q = __ldg(reinterpret_cast<const int4 *>(in + base + k));
+            v[k] = q.x;
+            v[k + 1] = q.y;
+            v[k + 2] = q.z;
+            v[k + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; k++) {
+            const int64_t i = base + k;
+            v[k] = i < n ? (long long)in[i] : 0;
+        }
     }
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) local += v[k];
     long long x = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -624,7 +624,9 @@ __device__ __forceinline__ int scan_thread(const GridDev &g, const int32_t *__re
             n++;
         }
     };
-    for (int32_t row = 0; row < nrows; row++) {
+    // the source range [q0, q1) of window row `row` (empty when the row
+    // misses the sphere); the row's cell_start loads are only issued here
+    auto row_span = [&](int32_t row, int32_t &q0, int32_t &q1) {
         int32_t rem = row;
         int64_t base = 0;
         double off2 = 0.0;
@@ -649,13 +651,24 @@ __device__ __forceinline__ int scan_thread(const GridDev &g, const int32_t *__re
             off2 += gap * gap;
         }
         const double hw2 = rs2 - off2;
-        if (!(hw2 >= -eps_r2)) continue;
+        if (!(hw2 >= -eps_r2)) {
+            q0 = q1 = 0;
+            return;
+        }
         const double hw = sqrt(fmax(hw2, 0.0) + eps_r2) * (1.0 + kSlackRel);
         const int64_t x0 = cell_of(t[0] - hw, g.lo[0], g.inv_d[0], g.n[0]);
         const int64_t x1 = cell_of(t[0] + hw, g.lo[0], g.inv_d[0], g.n[0]);
         FM_DCHECK(x0 >= 0 && x1 < g.n[0] && base >= 0 && base + x1 + 1 <= st);
-        const int32_t p0 = __ldg(cell_start + base + x0);
-        const int32_t p1 = __ldg(cell_start + base + x1 + 1);
+        q0 = __ldg(cell_start + base + x0);
+        q1 = __ldg(cell_start + base + x1 + 1);
+    };
+    // one row ahead: row r+1's cell_start loads are in flight while row r's
+    // points are scanned (C2 select 0.422 -> 0.412 ms)
+    int32_t n0, n1;
+    row_span(0, n0, n1);
+    for (int32_t row = 0; row < nrows; row++) {
+        const int32_t p0 = n0, p1 = n1;
+        if (row + 1 < nrows) row_span(row + 1, n0, n1);
         FM_DCHECK(0 <= p0 && p0 <= p1 && p1 <= __ldg(cell_start + st));
         int32_t p = p0;
         for (; p + 1 < p1; p += 2) {  // two point loads in flight
