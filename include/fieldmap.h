@@ -266,10 +266,11 @@ int fm_bucket_positions(const int32_t *counts, const int32_t *perm, int64_t p0, 
                         int32_t slot_cap, int32_t *bucket_list, int64_t bucket_stride,
                         int32_t *bucket_count, fm_stream_t stream);
 
-/* fm_offsets_ordered with every row length capped at slot_cap when
- * cap_rows != 0: the offsets then never exceed n * slot_cap (storage sized
- * without reading the counts back -- rows of overflowing supports get
- * slot_cap garbage entries; the caller detects them from the select stats). */
+/* fm_offsets_ordered for a sync-free step when cap_rows != 0: rows of
+ * supports larger than slot_cap get length 0, so the offsets never exceed
+ * n * slot_cap (storage sized without reading the counts back) and the apply
+ * writes 0 for those targets; the caller detects them from the select stats
+ * (stats[6]) and redoes the step through the re-gather path. */
 int fm_offsets_ordered_capped(const int32_t *counts, const int32_t *perm, int64_t n,
                               int32_t slot_cap, int32_t cap_rows, int64_t *offsets,
                               int32_t *bucket_list, int32_t *bucket_count, void *workspace,

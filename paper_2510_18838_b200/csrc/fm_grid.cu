@@ -65,8 +65,8 @@ static int64_t order_keys(const fm_grid *grid) {
 // positions [n*b/nblocks, n*(b+1)/nblocks).
 template <int DIM>
 __global__ void k_order_keys(GridDev g, const double *__restrict__ pts, int64_t n,
-                             int32_t *__restrict__ keys, int32_t *__restrict__ counts,
-                             int nblocks, int64_t nkeys) {
+                             int32_t *__restrict__ keys, int32_t *__restrict__ rank,
+                             int32_t *__restrict__ counts, int nblocks, int64_t nkeys) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double p[DIM];
@@ -80,13 +80,14 @@ __global__ void k_order_keys(GridDev g, const double *__restrict__ pts, int64_t 
         }
         const int32_t c = (int32_t)(blk * nkeys + order_key<DIM>(g, p));
         keys[i] = c;
-        atomicAdd(&counts[c], 1);
+        rank[i] = atomicAdd(&counts[c], 1);
     }
 }
 
 template <int DIM>
 __global__ void k_cell_keys(GridDev g, const double *__restrict__ pts, int64_t n,
-                            int32_t *__restrict__ keys, int32_t *__restrict__ counts) {
+                            int32_t *__restrict__ keys, int32_t *__restrict__ rank,
+                            int32_t *__restrict__ counts) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double p[DIM];
@@ -94,19 +95,18 @@ __global__ void k_cell_keys(GridDev g, const double *__restrict__ pts, int64_t n
         for (int a = 0; a < DIM; a++) p[a] = pts[i * DIM + a];
         const int32_t c = (int32_t)cell_key<DIM>(g, p);
         keys[i] = c;
-        atomicAdd(&counts[c], 1);
+        rank[i] = atomicAdd(&counts[c], 1);
     }
 }
 
-__global__ void k_scatter(const int32_t *__restrict__ keys, int64_t n,
-                          const int32_t *__restrict__ start, int32_t *__restrict__ fill,
+// counting-sort placement: the point's rank in its cell came from the
+// counting atomic (arrival order; the cells are sorted by id afterwards)
+__global__ void k_scatter(const int32_t *__restrict__ keys, const int32_t *__restrict__ rank,
+                          int64_t n, const int32_t *__restrict__ start,
                           int32_t *__restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = keys[i];
-        const int32_t pos = start[c] + atomicAdd(&fill[c], 1);
-        out[pos] = (int32_t)i;
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[__ldg(start + __ldg(keys + i)) + __ldg(rank + i)] = (int32_t)i;
 }
 
 // ids ascending inside each cell (the lexsort tie order of locate.py:79),
@@ -239,8 +239,23 @@ __global__ void k_bbox_pair(const double *__restrict__ a, int64_t na, const doub
         mn[k] = INFINITY;
         mx[k] = -INFINITY;
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {  // four points' loads in flight
+        double v[4][DIM];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int k = 0; k < DIM; k++) v[u][k] = __ldg(pts + (i + u * stride) * DIM + k);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int k = 0; k < DIM; k++) {
+                mn[k] = fmin(mn[k], v[u][k]);
+                mx[k] = fmax(mx[k], v[u][k]);
+            }
+    }
+    for (; i < n; i += stride) {
 #pragma unroll
         for (int k = 0; k < DIM; k++) {
             const double v = pts[i * DIM + k];
@@ -283,15 +298,15 @@ __global__ void k_bbox_final(const unsigned long long *acc, int dim, double *loh
 
 template <int DIM>
 static int launch_keys(const GridDev &g, const double *pts, int64_t n, int32_t *keys,
-                       int32_t *counts, cudaStream_t s, bool order = false, int nblocks = 1,
-                       int64_t nkeys = 0) {
+                       int32_t *rank, int32_t *counts, cudaStream_t s, bool order = false,
+                       int nblocks = 1, int64_t nkeys = 0) {
     const int threads = 256;
     const int64_t blocks = n > 0 ? std::min<int64_t>((n + threads - 1) / threads, kSMs * 16) : 0;
     if (blocks && order)
-        k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts, nblocks,
-                                                                 nkeys);
+        k_order_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, rank, counts,
+                                                                 nblocks, nkeys);
     else if (blocks)
-        k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, counts);
+        k_cell_keys<DIM><<<(unsigned)blocks, threads, 0, s>>>(g, pts, n, keys, rank, counts);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
@@ -303,8 +318,8 @@ using namespace fm;
 extern "C" {
 
 size_t fm_grid_workspace(int64_t n, int64_t ncell) {
-    return align256(sizeof(int32_t) * (size_t)n)           // keys
-           + align256(sizeof(int32_t) * (size_t)ncell) * 2  // counts, fill
+    return align256(sizeof(int32_t) * (size_t)n) * 2     // keys, ranks
+           + align256(sizeof(int32_t) * (size_t)ncell)  // counts
            + align256(scan_workspace_bytes(ncell));
 }
 
@@ -320,20 +335,20 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
     char *w = (char *)workspace;
     int32_t *keys = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)n);
+    int32_t *rank = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)n);
     int32_t *counts = (int32_t *)w;
-    w += align256(sizeof(int32_t) * (size_t)ncell);
-    int32_t *fill = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)ncell);
     void *scan_ws = w;
     const GridDev g = to_dev(grid);
-    cudaMemsetAsync(counts, 0, (size_t)((char *)(fill + ncell) - (char *)counts), s);
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
     int rc;
     switch (grid->dim) {
-    case 1: rc = launch_keys<1>(g, pts, n, keys, counts, s); break;
-    case 2: rc = launch_keys<2>(g, pts, n, keys, counts, s); break;
-    case 3: rc = launch_keys<3>(g, pts, n, keys, counts, s); break;
-    case 4: rc = launch_keys<4>(g, pts, n, keys, counts, s); break;
-    default: rc = launch_keys<5>(g, pts, n, keys, counts, s); break;
+    case 1: rc = launch_keys<1>(g, pts, n, keys, rank, counts, s); break;
+    case 2: rc = launch_keys<2>(g, pts, n, keys, rank, counts, s); break;
+    case 3: rc = launch_keys<3>(g, pts, n, keys, rank, counts, s); break;
+    case 4: rc = launch_keys<4>(g, pts, n, keys, rank, counts, s); break;
+    default: rc = launch_keys<5>(g, pts, n, keys, rank, counts, s); break;
     }
     if (rc) return rc;
     rc = exclusive_scan<int32_t, int32_t>(counts, ncell, cell_start, scan_ws,
@@ -342,7 +357,7 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
     const int threads = 256;
     if (n > 0) {
         const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, kSMs * 16);
-        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, fill, sorted_ids);
+        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, rank, n, cell_start, sorted_ids);
     }
     {
         const unsigned blocks =
@@ -406,22 +421,22 @@ int fm_target_order_blocked(const fm_grid *grid, const double *targets, int64_t 
     char *w = (char *)workspace;
     int32_t *keys = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)nt);
+    int32_t *rank = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)nt);
     int32_t *counts = (int32_t *)w;
-    w += align256(sizeof(int32_t) * (size_t)ncell);
-    int32_t *fill = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)ncell);
     int32_t *start = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)(ncell + 1));
     void *scan_ws = w;
     const GridDev g = to_dev(grid);
-    cudaMemsetAsync(counts, 0, (size_t)((char *)(fill + ncell) - (char *)counts), s);
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)ncell, s);
     int rc;
     switch (grid->dim) {
-    case 1: rc = launch_keys<1>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
-    case 2: rc = launch_keys<2>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
-    case 3: rc = launch_keys<3>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
-    case 4: rc = launch_keys<4>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
-    default: rc = launch_keys<5>(g, targets, nt, keys, counts, s, true, nblocks, nkeys); break;
+    case 1: rc = launch_keys<1>(g, targets, nt, keys, rank, counts, s, true, nblocks, nkeys); break;
+    case 2: rc = launch_keys<2>(g, targets, nt, keys, rank, counts, s, true, nblocks, nkeys); break;
+    case 3: rc = launch_keys<3>(g, targets, nt, keys, rank, counts, s, true, nblocks, nkeys); break;
+    case 4: rc = launch_keys<4>(g, targets, nt, keys, rank, counts, s, true, nblocks, nkeys); break;
+    default: rc = launch_keys<5>(g, targets, nt, keys, rank, counts, s, true, nblocks, nkeys); break;
     }
     if (rc) return rc;
     rc = exclusive_scan<int32_t, int32_t>(counts, ncell, start, scan_ws,
@@ -430,7 +445,7 @@ int fm_target_order_blocked(const fm_grid *grid, const double *targets, int64_t 
     if (nt > 0) {
         const int threads = 256;
         const int64_t blocks = std::min<int64_t>((nt + threads - 1) / threads, kSMs * 16);
-        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, nt, start, fill, perm);
+        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, rank, nt, start, perm);
     }
     FM_CHECK_LAUNCH();
     return FM_OK;

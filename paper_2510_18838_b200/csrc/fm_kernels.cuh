@@ -744,7 +744,7 @@ static __global__ void __launch_bounds__(256) k_gather_counts(
             const int64_t j = base + it * 256 + threadIdx.x;
             const int64_t i = p0 + j;
             const int m = j < n ? __ldg(counts + (perm ? __ldg(perm + i) : i)) : 0;
-            if (j < n && out) out[j] = (row_cap > 0 && m > row_cap) ? row_cap : m;
+            if (j < n && out) out[j] = (row_cap > 0 && m > row_cap) ? 0 : m;
             b[it] = (j < n && m <= slot_cap) ? bucket_of(m) : -1;
             at[it] = 0;
             if (bucket_list) {
