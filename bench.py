@@ -387,7 +387,15 @@ def run_b200(args, rank, world, local_rank):
             raise SystemExit(f"graphed step not valid for this workload: {graph_check}")
         Y1, op, cnt, stats, _c = eager
         extra = (_c, Y1)
-        if not torch.equal(Y1, gt.Y):
+        if os.environ.get("FM_CELLS_PER_POINT"):
+            # a different grid density changes the supports' discovery order,
+            # i.e. the rounding of the fits: equal to ~1e-12, not bitwise
+            rel = ((Y1 - gt.Y).abs() / Y1.abs().clamp_min(1e-300)).max().item()
+            print(f"graph vs eager (cells_per_point differs): max rel {rel:.3e}",
+                  file=sys.stderr)
+            if not rel < 1e-9:
+                raise SystemExit("graphed and eager steps disagree")
+        elif not torch.equal(Y1, gt.Y):
             raise SystemExit("graphed and eager steps disagree")
         phase = {"graph (whole step)": phase.get("graph", 0.0)}
         phase.update({f"eager {k}": v * args.steps for k, v in ph1.items()})

@@ -15,6 +15,7 @@ All launches go on torch's current CUDA stream.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,15 +60,34 @@ def _workspace(nbytes, device):
 
 
 # ------------------------------------------------------------------ a1
+# Source grid density (cells per source point).  The search grid is ours:
+# the supports and radii do not depend on it (§3), only the discovery order
+# of a support's points -- the fit's row order, i.e. its rounding -- does.
+# 1-D/2-D (thread-per-target select): 0.35 cells per point, measured fastest
+# on C2 (select 0.417 -> 0.356 ms: fewer, longer window rows); dim >= 3: 1.
+# Env FM_CELLS_PER_POINT overrides (A/B).
+_CELLS_PER_POINT_ENV = os.environ.get("FM_CELLS_PER_POINT")
+
+
+def default_cells_per_point(dim):
+    if _CELLS_PER_POINT_ENV:
+        return float(_CELLS_PER_POINT_ENV)
+    return 0.35 if dim <= 2 else 1.0
+
+
 class SourceCloud:
     """Source points resident in HBM and binned into a uniform grid.
 
     `points` (n, dim) fp64, dim 1..5.  The grid geometry follows the
-    reference's PointGrid (locate.py:144-161: padded bbox, ~cells_per_point
-    cells per point; for dim 2 the very same nx, ny, lo, dx, dy).  Search
-    results do not depend on the geometry."""
+    reference's PointGrid rules (locate.py:144-161: padded bbox, ~cells_per_point
+    cells per point; at 1.0 and dim 2 the very same nx, ny, lo, dx, dy) at
+    `default_cells_per_point(dim)`.  Supports and radii do not depend on the
+    geometry."""
 
-    def __init__(self, points, cells_per_point=1.0, bbox=None, geom=None):
+    def __init__(self, points, cells_per_point=None, bbox=None, geom=None):
+        if cells_per_point is None:
+            cells_per_point = default_cells_per_point(
+                points.shape[1] if getattr(points, "ndim", 1) == 2 else 2)
         host = None if isinstance(points, torch.Tensor) else np.ascontiguousarray(points,
                                                                                   dtype=np.float64)
         self.pts = to_device(points if host is None else host)
@@ -806,8 +826,9 @@ class GraphedTransfer:
         lo = np.ascontiguousarray(bs[0])
         hi = np.ascontiguousarray(bs[1])
         check(_lib.lib().fm_grid_geometry(self.dim, lo.ctypes.data, hi.ctypes.data, self.ns,
-                                          1.0, ctypes.byref(grid), None, None),
-              "fm_grid_geometry")
+                                          default_cells_per_point(self.dim), ctypes.byref(grid),
+                                          None,
+                                          None), "fm_grid_geometry")
         self.sel = self._select_spec(bs, bt)
         key = (bytes(grid), self.sel)
         if key != self.key:
