@@ -132,6 +132,16 @@ int fm_bbox(int dim, const double *pts, int64_t n, double *lohi, fm_stream_t str
 int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t nb,
                  double *lohi_host, void *workspace, fm_stream_t stream);
 
+/* fm_bbox_pair without the host round trip: enqueues the reduction and an
+ * asynchronous copy of 4*dim order-preserving keys into keys_host (pinned
+ * host memory; valid once the stream has passed this point -- record an
+ * event); fm_bbox_decode (host only) turns them into fm_bbox_pair's lohi.
+ * Lets a caller queue work behind the bbox before knowing it (the graphed
+ * step replays optimistically and checks the geometry afterwards). */
+int fm_bbox_pair_async(int dim, const double *a, int64_t na, const double *b, int64_t nb,
+                       unsigned long long *keys_host, void *workspace, fm_stream_t stream);
+int fm_bbox_decode(int dim, const unsigned long long *keys_host, double *lohi_host);
+
 /* Host-only: the PointGrid geometry for a source bbox -- _pad_bbox
  * (locate.py:50-62) and _grid_shape (locate.py:34-47) for dim 2, cells of
  * equal side for other dims -- as an fm_grid (lo/hi_out: padded box, may be

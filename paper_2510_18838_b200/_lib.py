@@ -66,6 +66,8 @@ SIGNATURES = {
     "fm_grid_build": (c_i32, [P(FmGrid), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "fm_bbox": (c_i32, [c_i32, c_vp, c_i64, c_vp, c_vp]),
     "fm_bbox_pair": (c_i32, [c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "fm_bbox_pair_async": (c_i32, [c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "fm_bbox_decode": (c_i32, [c_i32, c_vp, c_vp]),
     "fm_grid_geometry": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_dbl, P(FmGrid), c_vp, c_vp]),
     "fm_order_workspace": (c_sz, [c_i64, P(FmGrid)]),
     "fm_target_order": (c_i32, [P(FmGrid), c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),

@@ -463,9 +463,9 @@ static double host_dval(unsigned long long k) {
     return v;
 }
 
-int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t nb,
-                 double *lohi_host, void *workspace, fm_stream_t stream) {
-    if (dim < 1 || dim > kMaxDim || na < 0 || nb < 0 || !lohi_host || !workspace)
+int fm_bbox_pair_async(int dim, const double *a, int64_t na, const double *b, int64_t nb,
+                       unsigned long long *keys_host, void *workspace, fm_stream_t stream) {
+    if (dim < 1 || dim > kMaxDim || na < 0 || nb < 0 || !keys_host || !workspace)
         return FM_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *acc = reinterpret_cast<unsigned long long *>(workspace);
@@ -484,16 +484,29 @@ int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t 
     default: k_bbox_pair<5><<<grid, threads, 0, s>>>(a, na, b, nb, acc); break;
     }
     FM_CHECK_LAUNCH();
-    unsigned long long h[4 * kMaxDim];
-    if (cudaMemcpyAsync(h, acc, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
+    if (cudaMemcpyAsync(keys_host, acc, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
         return FM_ERR_CUDA;
+    return FM_OK;
+}
+
+int fm_bbox_decode(int dim, const unsigned long long *keys_host, double *lohi_host) {
+    if (dim < 1 || dim > kMaxDim || !keys_host || !lohi_host) return FM_ERR_ARG;
     for (int arr = 0; arr < 2; arr++)
         for (int k = 0; k < dim; k++) {
-            lohi_host[arr * 2 * dim + k] = host_dval(h[arr * 2 * dim + k]);
-            lohi_host[arr * 2 * dim + dim + k] = host_dval(~h[arr * 2 * dim + dim + k]);
+            lohi_host[arr * 2 * dim + k] = host_dval(keys_host[arr * 2 * dim + k]);
+            lohi_host[arr * 2 * dim + dim + k] = host_dval(~keys_host[arr * 2 * dim + dim + k]);
         }
     return FM_OK;
+}
+
+int fm_bbox_pair(int dim, const double *a, int64_t na, const double *b, int64_t nb,
+                 double *lohi_host, void *workspace, fm_stream_t stream) {
+    if (!lohi_host) return FM_ERR_ARG;
+    unsigned long long h[4 * kMaxDim];
+    const int rc = fm_bbox_pair_async(dim, a, na, b, nb, h, workspace, stream);
+    if (rc) return rc;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return FM_ERR_CUDA;
+    return fm_bbox_decode(dim, h, lohi_host);
 }
 
 /* locate.py:50-62 (_pad_bbox) and 34-47 (_grid_shape) in C, for any dim
