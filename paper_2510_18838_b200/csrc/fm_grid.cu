@@ -109,10 +109,7 @@ __global__ void k_scatter(const int32_t *__restrict__ keys, const int32_t *__res
         out[__ldg(start + __ldg(keys + i)) + __ldg(rank + i)] = (int32_t)i;
 }
 
-// ids ascending inside each cell (the lexsort tie order of locate.py:79),
-// then the cell's coordinates gathered into cell order.  One thread per cell:
-// insertion sort for the usual handful of points, heapsort for crowded cells
-// (clustered or coincident sources) so the cost stays n log n.
+// heapsort helper of k_place (crowded cells)
 __device__ __forceinline__ void sift_down(int32_t *a, int32_t root, int32_t n) {
     for (;;) {
         int32_t c = 2 * root + 1;
@@ -126,38 +123,47 @@ __device__ __forceinline__ void sift_down(int32_t *a, int32_t root, int32_t n) {
     }
 }
 
+// One thread per source point: its place in its cell is the number of the
+// cell's points with a smaller id (the scatter left them in arrival order in
+// `arrival`), so ids come out ascending per cell (the lexsort tie order of
+// locate.py:79) and the point's coordinates go straight to their slot.
+// A cell of more than kPlaceMax points (clustered or coincident sources) is
+// sorted by ONE thread -- the one whose point arrived first -- with heapsort,
+// so the cost stays n log n instead of k^2 per cell.
+constexpr int kPlaceMax = 64;
 template <int DIM>
-__global__ void k_sort_cells(const int32_t *__restrict__ start, int64_t ncell,
-                             int32_t *__restrict__ ids, const double *__restrict__ pts,
-                             double *__restrict__ sorted_pts) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = start[c], e = start[c + 1];
-        if (e - b <= 16) {
-            for (int32_t i = b + 1; i < e; i++) {
-                const int32_t v = ids[i];
-                int32_t j = i - 1;
-                while (j >= b && ids[j] > v) {
-                    ids[j + 1] = ids[j];
-                    j--;
-                }
-                ids[j + 1] = v;
-            }
-        } else {
-            int32_t *a = ids + b;
-            const int32_t n = e - b;
-            for (int32_t r = n / 2 - 1; r >= 0; r--) sift_down(a, r, n);
-            for (int32_t m = n - 1; m > 0; m--) {
-                const int32_t t = a[0];
-                a[0] = a[m];
-                a[m] = t;
-                sift_down(a, 0, m);
-            }
-        }
-        for (int32_t i = b; i < e; i++) {
-            const int64_t sidx = ids[i];
+__global__ void k_place(const int32_t *__restrict__ keys, int64_t n,
+                        const int32_t *__restrict__ start, const int32_t *__restrict__ arrival,
+                        const double *__restrict__ pts, int32_t *__restrict__ ids,
+                        double *__restrict__ sorted_pts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = __ldg(keys + i);
+        const int32_t b = __ldg(start + c), e = __ldg(start + c + 1);
+        if (e - b <= kPlaceMax) {
+            int32_t r = 0;
+            for (int32_t q = b; q < e; q++) r += __ldg(arrival + q) < (int32_t)i;
+            const int64_t p = b + r;
+            ids[p] = (int32_t)i;
 #pragma unroll
-            for (int a = 0; a < DIM; a++) sorted_pts[(int64_t)i * DIM + a] = pts[sidx * DIM + a];
+            for (int a = 0; a < DIM; a++) sorted_pts[p * DIM + a] = __ldg(pts + i * DIM + a);
+        } else if (__ldg(arrival + b) == (int32_t)i) {
+            int32_t *v = ids + b;
+            const int32_t m = e - b;
+            for (int32_t q = 0; q < m; q++) v[q] = arrival[b + q];
+            for (int32_t r = m / 2 - 1; r >= 0; r--) sift_down(v, r, m);
+            for (int32_t k = m - 1; k > 0; k--) {
+                const int32_t t = v[0];
+                v[0] = v[k];
+                v[k] = t;
+                sift_down(v, 0, k);
+            }
+            for (int32_t q = 0; q < m; q++) {
+                const int64_t sidx = v[q];
+#pragma unroll
+                for (int a = 0; a < DIM; a++)
+                    sorted_pts[(int64_t)(b + q) * DIM + a] = pts[sidx * DIM + a];
+            }
         }
     }
 }
@@ -318,7 +324,7 @@ using namespace fm;
 extern "C" {
 
 size_t fm_grid_workspace(int64_t n, int64_t ncell) {
-    return align256(sizeof(int32_t) * (size_t)n) * 2     // keys, ranks
+    return align256(sizeof(int32_t) * (size_t)n) * 3     // keys, ranks, arrival order
            + align256(sizeof(int32_t) * (size_t)ncell)  // counts
            + align256(scan_workspace_bytes(ncell));
 }
@@ -336,6 +342,8 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
     int32_t *keys = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)n);
     int32_t *rank = (int32_t *)w;
+    w += align256(sizeof(int32_t) * (size_t)n);
+    int32_t *arrival = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)n);
     int32_t *counts = (int32_t *)w;
     w += align256(sizeof(int32_t) * (size_t)ncell);
@@ -357,17 +365,13 @@ int fm_grid_build(const fm_grid *grid, const double *pts, int64_t n, int32_t *ce
     const int threads = 256;
     if (n > 0) {
         const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, kSMs * 16);
-        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, rank, n, cell_start, sorted_ids);
-    }
-    {
-        const unsigned blocks =
-            (unsigned)std::min<int64_t>((ncell + threads - 1) / threads, kSMs * 16);
+        k_scatter<<<(unsigned)blocks, threads, 0, s>>>(keys, rank, n, cell_start, arrival);
         switch (grid->dim) {
-        case 1: k_sort_cells<1><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
-        case 2: k_sort_cells<2><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
-        case 3: k_sort_cells<3><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
-        case 4: k_sort_cells<4><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
-        default: k_sort_cells<5><<<blocks, threads, 0, s>>>(cell_start, ncell, sorted_ids, pts, sorted_pts); break;
+        case 1: k_place<1><<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, arrival, pts, sorted_ids, sorted_pts); break;
+        case 2: k_place<2><<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, arrival, pts, sorted_ids, sorted_pts); break;
+        case 3: k_place<3><<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, arrival, pts, sorted_ids, sorted_pts); break;
+        case 4: k_place<4><<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, arrival, pts, sorted_ids, sorted_pts); break;
+        default: k_place<5><<<(unsigned)blocks, threads, 0, s>>>(keys, n, cell_start, arrival, pts, sorted_ids, sorted_pts); break;
         }
     }
     FM_CHECK_LAUNCH();

@@ -119,12 +119,33 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(
     }
     __syncthreads();
     long long run = s_prefix + (x - local) + (wid > 0 ? warp_tot[wid - 1] : 0);
+    if (vec && ((uintptr_t)out & 15) == 0) {  // full tile: 16-byte stores
+        TOut o[kScanItems];
 #pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        const int64_t i = base + k;
-        if (i < n) out[i] = (TOut)run;
-        run += v[k];
-        if (i == n - 1) out[n] = (TOut)run;
+        for (int k = 0; k < kScanItems; k++) {
+            o[k] = (TOut)run;
+            run += v[k];
+        }
+        if constexpr (sizeof(TOut) == 4) {
+#pragma unroll
+            for (int k = 0; k < kScanItems; k += 4)
+                *reinterpret_cast<int4 *>(out + base + k) =
+                    make_int4((int)o[k], (int)o[k + 1], (int)o[k + 2], (int)o[k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kScanItems; k += 2)
+                *reinterpret_cast<longlong2 *>(out + base + k) =
+                    make_longlong2((long long)o[k], (long long)o[k + 1]);
+        }
+        if (base + kScanItems == n) out[n] = (TOut)run;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; k++) {
+            const int64_t i = base + k;
+            if (i < n) out[i] = (TOut)run;
+            run += v[k];
+            if (i == n - 1) out[n] = (TOut)run;
+        }
     }
 }
 

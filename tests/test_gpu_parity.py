@@ -1046,3 +1046,64 @@ def test_graphed_transfer_equals_eager():
     gt2.run()
     chk = gt2.check()
     assert chk["overflow"] > 0 and not chk["valid"]
+
+
+@pytest.mark.gpu
+def test_scan_tiles_and_edges():
+    """The single-pass look-back scan (fm_scan.cuh) through fm_offsets_from_counts:
+    exact int64 offsets for empty, one-element, partial-tile, exact multiples of
+    the 8192-element tile (vector stores + the closing total), misaligned
+    inputs (scalar path) and a 3M-element input with large counts."""
+    import torch
+
+    from paper_2510_18838_b200 import _lib
+    from paper_2510_18838_b200.device import _stream
+
+    L = _lib.lib()
+    rs = np.random.RandomState(7)
+    for n in (0, 1, 5, 8191, 8192, 8193, 16384, 3 * 8192 + 17, 3_000_000):
+        for shift in ((0, 1) if n else (0,)):
+            c = rs.randint(0, 1000 if n < 10**6 else 2000, n + shift).astype(np.int32)
+            cd = torch.from_numpy(c).cuda()[shift:]  # shift 1: a 4-byte misaligned input
+            off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            ws_bytes = L.fm_scan_workspace(n)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+            _lib.check(L.fm_offsets_from_counts(_lib.ptr(cd) if n else None, n, _lib.ptr(off),
+                                                _lib.ptr(ws), ws_bytes, _stream()),
+                       "fm_offsets_from_counts")
+            want = np.concatenate([[0], np.cumsum(c[shift:].astype(np.int64))])
+            assert np.array_equal(off.cpu().numpy(), want), (n, shift)
+
+
+@pytest.mark.gpu
+def test_grid_binning_crowded_and_coincident_cells():
+    """fm_grid_build's cell CSR (counting sort + in-cell id order) against a
+    numpy restatement of the same cell formula (trunc(fl(p - lo) * inv_d),
+    clamped; ids ascending per cell, the lexsort order of locate.py:79), at
+    the default density, at the reference's 1 cell per point, and at 0.01
+    cells per point (~100 points per cell: the heapsort path for cells of
+    more than 64 points), with 3000 coincident duplicates in one cell."""
+    from paper_2510_18838_b200 import device as D
+
+    rs = np.random.RandomState(11)
+    src = np.concatenate([rs.uniform(0, 1, (20000, 2)),
+                          np.tile([[0.3, 0.7]], (3000, 1)),
+                          rs.normal(0.6, 1e-3, (2000, 2))])
+    src = src[rs.permutation(src.shape[0])]
+    for cpp in (None, 1.0, 0.01):
+        cloud = D.SourceCloud(src, cells_per_point=cpp)
+        g = cloud.grid
+        cells = np.zeros(src.shape[0], dtype=np.int64)
+        stride = 1
+        for a in range(2):
+            ia = np.trunc((src[:, a] - g.lo[a]) * g.inv_d[a]).astype(np.int64)
+            cells += np.clip(ia, 0, g.n[a] - 1) * stride
+            stride *= g.n[a]
+        ids = np.arange(src.shape[0])
+        order = np.lexsort((ids, cells))
+        start = np.zeros(g.ncell + 1, dtype=np.int64)
+        np.add.at(start, cells + 1, 1)
+        np.cumsum(start, out=start)
+        assert np.array_equal(cloud.cell_start.cpu().numpy(), start), cpp
+        assert np.array_equal(cloud.sorted_ids.cpu().numpy(), ids[order]), cpp
+        assert np.array_equal(cloud.sorted_pts.cpu().numpy(), src[order]), cpp
