@@ -44,13 +44,15 @@ __global__ void k_scale_points(const double *__restrict__ pts, int64_t n, int di
 // 0.150 vs 0.178 / 0.234 / 0.377 ms on C2 -- the per-pass overhead outweighs
 // the L1 left to cache X); CS = evict-first (col, val) loads (no gain).
 // A variant double-buffering the next tile's (col, val) with cp.async was
-// slower (0.166 ms): the kernel is bound by L1 wavefronts, not by latency.
+// slower (0.166 ms): the kernel is bound by L1 wavefronts, not by latency;
+// so was (col, val) staged as 16-byte records read with one shared load per
+// nonzero (0.186 ms: 32 KB of staging per block, weights held in registers).
 #ifdef FM_APPLY_MINB
 #define FM_APPLY_BOUNDS __launch_bounds__(256, FM_APPLY_MINB)
 #else
 #define FM_APPLY_BOUNDS __launch_bounds__(256)
 #endif
-template <int L, int V, int CH, bool REC>
+template <int L, int V, int CH, bool CS>
 __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
                                                const int32_t *__restrict__ col,
                                                const double *__restrict__ val,
@@ -63,18 +65,13 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
 #define FM_APPLY_U 8
 #endif
     constexpr int U = FM_APPLY_U;
-    // REC: (col, val) staged as one 16-byte record per nonzero, read with
-    // ONE shared load per nonzero and lane group instead of two
-    constexpr int SC = REC ? 1 : CH, SR = REC ? CH : 1;
-    __shared__ int32_t s_col[8][SC];
-    __shared__ double s_val[8][SC];
-    __shared__ int4 s_rec[8][SR];
+    __shared__ int32_t s_col[8][CH];
+    __shared__ double s_val[8][CH];
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int rr = lane / L, li = lane % L;
     int32_t *sc = s_col[wib];
     double *sv = s_val[wib];
-    int4 *sr = s_rec[wib];
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t tile = warp; tile * RPW < nrows; tile += nwarps) {
@@ -91,31 +88,18 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
         for (int64_t cs = tb; cs < te; cs += CH) {
             const int n = (int)(te - cs < CH ? te - cs : CH);
             for (int i = lane; i < n; i += 32) {
-                if constexpr (REC) {
-                    const double w = __ldg(val + cs + i);
-                    sr[i] = make_int4(__ldg(col + cs + i), 0, __double2loint(w), __double2hiint(w));
-                } else {
-                    sc[i] = __ldg(col + cs + i);
-                    sv[i] = __ldg(val + cs + i);
-                }
+                sc[i] = CS ? __ldcs(col + cs + i) : __ldg(col + cs + i);
+                sv[i] = CS ? __ldcs(val + cs + i) : __ldg(val + cs + i);
             }
             __syncwarp();
             const int j0 = (int)((rb > cs ? rb : cs) - cs);
             const int j1 = (int)((re < cs + n ? re : cs + n) - cs);
             int j = j0;
             for (; j + U <= j1; j += U) {
-                double x[U][V], w[U];
+                double x[U][V];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    int cj;
-                    if constexpr (REC) {
-                        const int4 q = sr[j + u];
-                        cj = q.x;
-                        w[u] = __hiloint2double(q.w, q.z);
-                    } else {
-                        cj = sc[j + u];
-                    }
-                    const double *xp = X + (int64_t)cj * C + li * V;
+                    const double *xp = X + (int64_t)sc[j + u] * C + li * V;
                     if (V == 2) {
                         const double2 x2 = __ldg(reinterpret_cast<const double2 *>(xp));
                         x[u][0] = x2.x;
@@ -126,26 +110,14 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const double wu = REC ? w[u] : sv[j + u];
+                for (int u = 0; u < U; u++)
 #pragma unroll
-                    for (int v = 0; v < V; v++) acc[v] = fma(wu, x[u][v], acc[v]);
-                }
+                    for (int v = 0; v < V; v++) acc[v] = fma(sv[j + u], x[u][v], acc[v]);
             }
             for (; j < j1; j++) {
-                int cj;
-                double wj;
-                if constexpr (REC) {
-                    const int4 q = sr[j];
-                    cj = q.x;
-                    wj = __hiloint2double(q.w, q.z);
-                } else {
-                    cj = sc[j];
-                    wj = sv[j];
-                }
-                const double *xp = X + (int64_t)cj * C + li * V;
+                const double *xp = X + (int64_t)sc[j] * C + li * V;
 #pragma unroll
-                for (int v = 0; v < V; v++) acc[v] = fma(wj, __ldg(xp + v), acc[v]);
+                for (int v = 0; v < V; v++) acc[v] = fma(sv[j], __ldg(xp + v), acc[v]);
             }
             __syncwarp();
         }
@@ -180,15 +152,7 @@ __global__ void k_apply_generic(int64_t nrows, const int64_t *__restrict__ row_o
     }
 }
 
-static bool apply_rec() {  // A/B switch: env FM_APPLY_REC=0/1
-    static const bool v = [] {
-        const char *e = getenv("FM_APPLY_REC");
-        return e && atoi(e) != 0;
-    }();
-    return v;
-}
-
-template <int L, int V, int CH = 256>
+template <int L, int V, int CH = 256, bool CS = false>
 static int launch_apply(int64_t nrows, const int64_t *row_off, const int32_t *col,
                         const double *val, const int32_t *row_target, const double *X, double *Y,
                         cudaStream_t st) {
@@ -197,10 +161,7 @@ static int launch_apply(int64_t nrows, const int64_t *row_off, const int32_t *co
     const int64_t tiles = (nrows + RPW - 1) / RPW;
     const int64_t need = (tiles + 7) / 8;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kSMs * 8));
-    if (apply_rec())
-        k_apply<L, V, CH, true><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
-    else
-        k_apply<L, V, CH, false><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
+    k_apply<L, V, CH, CS><<<blocks, threads, 0, st>>>(nrows, row_off, col, val, row_target, X, Y);
     FM_CHECK_LAUNCH();
     return FM_OK;
 }
