@@ -123,34 +123,37 @@ __device__ __forceinline__ void sift_down(int32_t *a, int32_t root, int32_t n) {
     }
 }
 
-// One thread per source point: its place in its cell is the number of the
-// cell's points with a smaller id (the scatter left them in arrival order in
-// `arrival`), so ids come out ascending per cell (the lexsort tie order of
-// locate.py:79) and the point's coordinates go straight to their slot.
+// One thread per cell-order position q (the scatter left the cell's points
+// there in arrival order): the point i = arrival[q] goes to its place in the
+// cell, the number of the cell's points with a smaller id, so ids come out
+// ascending per cell (the lexsort tie order of locate.py:79) and its
+// coordinates go straight to their slot.  Walking positions, not point ids,
+// keeps the reads and writes local for any input order (random clouds).
 // A cell of more than kPlaceMax points (clustered or coincident sources) is
-// sorted by ONE thread -- the one whose point arrived first -- with heapsort,
-// so the cost stays n log n instead of k^2 per cell.
+// sorted by ONE thread -- the one at its first position -- with heapsort, so
+// the cost stays n log n instead of k^2 per cell.
 constexpr int kPlaceMax = 64;
 template <int DIM>
 __global__ void k_place(const int32_t *__restrict__ keys, int64_t n,
                         const int32_t *__restrict__ start, const int32_t *__restrict__ arrival,
                         const double *__restrict__ pts, int32_t *__restrict__ ids,
                         double *__restrict__ sorted_pts) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = __ldg(arrival + q);
         const int32_t c = __ldg(keys + i);
         const int32_t b = __ldg(start + c), e = __ldg(start + c + 1);
         if (e - b <= kPlaceMax) {
             int32_t r = 0;
-            for (int32_t q = b; q < e; q++) r += __ldg(arrival + q) < (int32_t)i;
+            for (int32_t k = b; k < e; k++) r += __ldg(arrival + k) < i;
             const int64_t p = b + r;
-            ids[p] = (int32_t)i;
+            ids[p] = i;
 #pragma unroll
-            for (int a = 0; a < DIM; a++) sorted_pts[p * DIM + a] = __ldg(pts + i * DIM + a);
-        } else if (__ldg(arrival + b) == (int32_t)i) {
+            for (int a = 0; a < DIM; a++) sorted_pts[p * DIM + a] = __ldg(pts + (int64_t)i * DIM + a);
+        } else if (q == b) {
             int32_t *v = ids + b;
             const int32_t m = e - b;
-            for (int32_t q = 0; q < m; q++) v[q] = arrival[b + q];
+            for (int32_t k = 0; k < m; k++) v[k] = arrival[b + k];
             for (int32_t r = m / 2 - 1; r >= 0; r--) sift_down(v, r, m);
             for (int32_t k = m - 1; k > 0; k--) {
                 const int32_t t = v[0];
@@ -158,11 +161,11 @@ __global__ void k_place(const int32_t *__restrict__ keys, int64_t n,
                 v[k] = t;
                 sift_down(v, 0, k);
             }
-            for (int32_t q = 0; q < m; q++) {
-                const int64_t sidx = v[q];
+            for (int32_t k = 0; k < m; k++) {
+                const int64_t sidx = v[k];
 #pragma unroll
                 for (int a = 0; a < DIM; a++)
-                    sorted_pts[(int64_t)(b + q) * DIM + a] = pts[sidx * DIM + a];
+                    sorted_pts[(int64_t)(b + k) * DIM + a] = pts[sidx * DIM + a];
             }
         }
     }
