@@ -203,7 +203,7 @@ def fit_flops(counts, k):
 # kernels launched by one device step (our own, counted from the launch
 # sequence in device.py / libfieldmap.so and checked against the ncu launch
 # list, profiles/): bbox pair 1; grid build: cell keys, scan, scatter,
-# in-cell sort 4; target order: keys, scan, scatter 3; select: stats init +
+# in-cell placement 4; target order: keys, scan, scatter 3; select: stats init +
 # select 2; ordered offsets: gather counts + scan 2; build: stats init + one
 # per non-empty size bucket (+1 if some support overflows its slot); apply 1
 def launches_per_step(sel):
@@ -500,8 +500,10 @@ def run_b200(args, rank, world, local_rank):
         "parallelism": f"target-sharded x{world}" + (
             " + NCCL all-gather of the target field" if world > 1 else ""),
         "phases_ms_per_step": {k2: v / args.steps for k2, v in phase.items()},
+        # graphed step: bbox 1, binning 4, order 3, stats init + fused
+        # select/buckets 2, offsets scan 1, build stats init 1, buckets, apply 1
         "gpu_launches": (launches_per_step(cnt) if gt is None else
-                         14 + bin(gt.mask).count("1")) * args.steps,
+                         13 + bin(gt.mask).count("1")) * args.steps,
         "graph": graph_check,
         "roofline": {
             "kernel": "k_build (C4 weights + Householder QR + operator row, supports from k_select)",

@@ -250,6 +250,25 @@ int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const dou
                        int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
                        void *pos_info, double *pos_targets, fm_stream_t stream);
 
+/* fm_select_supports fused with what fm_offsets_ordered(_capped) derives
+ * from its counts, for a step with no host round trip between the select
+ * and the build: pos_counts[k] = the row length of position k (its support
+ * size; 0 for a support beyond slot_cap when cap_rows != 0) -- scan it with
+ * fm_offsets_from_counts for the row offsets -- and the size buckets
+ * (bucket_list stride nt, bucket_count device int32[FM_NBUCKETS], zeroed by
+ * the call) exactly as fm_offsets_ordered writes them (order within a bucket
+ * unspecified).  1-D/2-D: written by the select kernel itself; dim >= 3: a
+ * separate gather pass after it. */
+int fm_select_supports_bucketed(const fm_grid *grid, const int32_t *cell_start,
+                                const double *sorted_pts, const int32_t *sorted_ids,
+                                const double *targets, int64_t nt, const int32_t *perm,
+                                const fm_select *sel, int32_t min_required, int32_t *counts,
+                                double *radii, uint8_t *status, int32_t *slot_id,
+                                int32_t *slot_pos, int32_t slot_cap, int32_t *overflow,
+                                int32_t *stats, void *pos_info, double *pos_targets,
+                                int32_t cap_rows, int32_t *pos_counts, int32_t *bucket_list,
+                                int32_t *bucket_count, fm_stream_t stream);
+
 /* Row offsets of an operator stored in processing order:
  * offsets[k+1] = offsets[k] + counts[perm[k]] (perm may be NULL).
  * Optionally (bucket_list != NULL) also partitions the positions by support

@@ -87,6 +87,10 @@ SIGNATURES = {
     "fm_select_supports": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, P(FmSelect),
                                    c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                                    c_vp, c_vp]),
+    "fm_select_supports_bucketed": (c_i32, [P(FmGrid), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                            P(FmSelect), c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                            c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
+                                            c_vp, c_vp]),
     "fm_offsets_ordered_workspace": (c_sz, [c_i64]),
     "fm_offsets_ordered_capped": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp,
                                           c_vp, c_sz, c_vp]),

@@ -484,12 +484,13 @@ int fm_transfer_values(const fm_grid *grid, const int32_t *cell_start, const dou
                         status, stats, true, stream);
 }
 
-int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
-                       const int32_t *sorted_ids, const double *targets, int64_t nt,
-                       const int32_t *perm, const fm_select *sel, int32_t min_required,
-                       int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
-                       int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
-                       void *pos_info, double *pos_targets, fm_stream_t stream) {
+static int select_dispatch(const fm_grid *grid, const int32_t *cell_start,
+                           const double *sorted_pts, const int32_t *sorted_ids,
+                           const double *targets, int64_t nt, const int32_t *perm,
+                           const fm_select *sel, int32_t min_required, int32_t *counts,
+                           double *radii, uint8_t *status, int32_t *slot_id, int32_t *slot_pos,
+                           int32_t slot_cap, int32_t *overflow, int32_t *stats, void *pos_info,
+                           double *pos_targets, fm_stream_t stream, const SelectBuckets &bk) {
     if (!grid_ok(grid) || !sel || nt < 0 || slot_cap < 1 || !stats || !overflow || !counts)
         return FM_ERR_ARG;
     if (sel->adaptive ? !(sel->r0 > 0.0 && sel->growth > 1.0 && sel->min_pts >= 1 && radii)
@@ -500,12 +501,58 @@ int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const dou
     cudaStream_t st = (cudaStream_t)stream;
     PosInfo *pi = reinterpret_cast<PosInfo *>(pos_info);
     switch (grid->dim) {
-    case 1: return dim1_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
-    case 2: return dim2_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
-    case 3: return dim3_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
-    case 4: return dim4_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
-    default: return dim5_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st);
+    case 1: return dim1_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st, bk);
+    case 2: return dim2_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st, bk);
+    case 3: return dim3_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st, bk);
+    case 4: return dim4_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st, bk);
+    default: return dim5_select(s, min_required, counts, radii, status, slot_id, slot_pos, slot_cap, overflow, stats, pi, pos_targets, st, bk);
     }
+}
+
+int fm_select_supports(const fm_grid *grid, const int32_t *cell_start, const double *sorted_pts,
+                       const int32_t *sorted_ids, const double *targets, int64_t nt,
+                       const int32_t *perm, const fm_select *sel, int32_t min_required,
+                       int32_t *counts, double *radii, uint8_t *status, int32_t *slot_id,
+                       int32_t *slot_pos, int32_t slot_cap, int32_t *overflow, int32_t *stats,
+                       void *pos_info, double *pos_targets, fm_stream_t stream) {
+    return select_dispatch(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel,
+                           min_required, counts, radii, status, slot_id, slot_pos, slot_cap,
+                           overflow, stats, pos_info, pos_targets, stream,
+                           SelectBuckets{nullptr, nullptr, nullptr, 0});
+}
+
+int fm_select_supports_bucketed(const fm_grid *grid, const int32_t *cell_start,
+                                const double *sorted_pts, const int32_t *sorted_ids,
+                                const double *targets, int64_t nt, const int32_t *perm,
+                                const fm_select *sel, int32_t min_required, int32_t *counts,
+                                double *radii, uint8_t *status, int32_t *slot_id,
+                                int32_t *slot_pos, int32_t slot_cap, int32_t *overflow,
+                                int32_t *stats, void *pos_info, double *pos_targets,
+                                int32_t cap_rows, int32_t *pos_counts, int32_t *bucket_list,
+                                int32_t *bucket_count, fm_stream_t stream) {
+    if (!pos_counts || !bucket_list || !bucket_count) return FM_ERR_ARG;
+    const SelectBuckets bk{pos_counts, bucket_list, bucket_count, cap_rows};
+    int rc = select_dispatch(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel,
+                             min_required, counts, radii, status, slot_id, slot_pos, slot_cap,
+                             overflow, stats, pos_info, pos_targets, stream, bk);
+    if (rc != FM_ERR_UNSUPPORTED) return rc;
+    // lane-group select (dim >= 3): the plain select, then the same outputs
+    // from a separate gather pass
+    rc = fm_select_supports(grid, cell_start, sorted_pts, sorted_ids, targets, nt, perm, sel,
+                            min_required, counts, radii, status, slot_id, slot_pos, slot_cap,
+                            overflow, stats, pos_info, pos_targets, stream);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(bucket_count, 0, sizeof(int32_t) * FM_NBUCKETS, st) != cudaSuccess)
+        return FM_ERR_CUDA;
+    if (nt > 0) {
+        const int blocks = (int)std::min<int64_t>((nt + 1023) / 1024, (int64_t)kSMs * 8);
+        k_gather_counts<<<blocks, 256, 0, st>>>(counts, perm, nt, pos_counts, slot_cap,
+                                                bucket_list, bucket_count, 0, -1,
+                                                cap_rows ? slot_cap : 0);
+        FM_CHECK_LAUNCH();
+    }
+    return FM_OK;
 }
 
 size_t fm_offsets_ordered_workspace(int64_t n) {

@@ -55,8 +55,10 @@ __device__ __forceinline__ void load_target(const double *__restrict__ targets, 
 // --------------------------------------------------------- stats helpers
 // stats arrays: pairs of (count, first index) plus min/max slots; written
 // with warp-aggregated atomics.
-static __global__ void k_stats_init(int32_t *stats, int n, int kind) {
+static __global__ void k_stats_init(int32_t *stats, int n, int kind,
+                                    int32_t *zero = nullptr, int nzero = 0) {
     const int i = threadIdx.x;
+    if (zero && i < nzero) zero[i] = 0;
     if (i >= n) return;
     if (kind == 0)  // count stats: max, min, nshort, first, nstatus, first
         stats[i] = (i == 1 || i == 3 || i == 5) ? INT32_MAX : 0;
@@ -610,6 +612,25 @@ __global__ void __launch_bounds__(kBlock, G == 8 ? 8 : 1) k_select(SearchArgs s,
     warp_flush_pair(stats + 4, nstat, first_stat);
 }
 
+// size bucket of a support (fieldmap.h FM_BUCKET_EDGES)
+__device__ __forceinline__ int bucket_of(int m) {
+    constexpr int edges[FM_NBUCKETS] = FM_BUCKET_EDGES;
+    int b = 0;
+#pragma unroll
+    for (int i = 0; i < FM_NBUCKETS - 1; i++) b += m > edges[i];
+    return b;
+}
+
+// Optional fused outputs of the thread select (fm_select_supports_bucketed):
+// per position the row length of the ordered offsets (0 for a support beyond
+// the slot when cap_rows) and the size-bucket lists of fm_offsets_ordered.
+struct SelectBuckets {
+    int32_t *pos_counts;    // NULL: not requested
+    int32_t *bucket_list;   // FM_NBUCKETS lists of stride nt
+    int32_t *bucket_count;  // zeroed before the launch
+    int cap_rows;
+};
+
 // Thread-per-target select pass (1-D / 2-D): same outputs as k_select.
 // The supports go from the per-thread shared-memory lists to the slots with
 // one coalesced warp store per target (lanes over entries).
@@ -625,7 +646,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
                                                      int32_t *__restrict__ overflow,
                                                      int32_t *__restrict__ stats,
                                                      PosInfo *__restrict__ pos_info,
-                                                     double *__restrict__ pos_t) {
+                                                     double *__restrict__ pos_t,
+                                                     SelectBuckets bk) {
     extern __shared__ __align__(16) char smem[];
     const int stride = lcap | 1;  // odd: a warp's appends spread over the banks
     int32_t *lpos_all = reinterpret_cast<int32_t *>(smem);
@@ -678,6 +700,18 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
                 first_short = min(first_short, (int)tid);
             }
         }
+        if (bk.pos_counts) {  // what fm_offsets_ordered(_capped) derives, fused
+            if (active) bk.pos_counts[k] = (bk.cap_rows && !slotted) ? 0 : m;
+            const int b = (active && slotted) ? bucket_of(m) : -1;
+            const unsigned peers = __match_any_sync(FM_FULL_MASK, b);
+            const int leader = __ffs(peers) - 1;
+            int at = 0;
+            if (lane == leader && b >= 0) at = atomicAdd(bk.bucket_count + b, __popc(peers));
+            at = __shfl_sync(FM_FULL_MASK, at, leader);
+            if (b >= 0)
+                bk.bucket_list[(int64_t)b * s.nt + at + __popc(peers & ((1u << lane) - 1u))] =
+                    (int32_t)k;
+        }
         __syncwarp();
         // supports -> slots: one target at a time, lanes over its entries
         const int mine = slotted ? m : 0;
@@ -708,14 +742,6 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
     warp_flush_pair(stats + 4, nstat, first_stat);
 }
 
-// size bucket of a support (fieldmap.h FM_BUCKET_EDGES)
-__device__ __forceinline__ int bucket_of(int m) {
-    constexpr int edges[FM_NBUCKETS] = FM_BUCKET_EDGES;
-    int b = 0;
-#pragma unroll
-    for (int i = 0; i < FM_NBUCKETS - 1; i++) b += m > edges[i];
-    return b;
-}
 
 // counts in processing order (input of the ordered offsets scan) and,
 // with bucket_list, the positions partitioned by support size.  Appends are
@@ -918,11 +944,12 @@ template <int DIM>
 int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, double *radii,
                   uint8_t *status, int32_t *slot_id, int32_t *slot_pos, int slot_cap,
                   int32_t *overflow, int32_t *stats, PosInfo *pos_info, double *pos_t,
-                  cudaStream_t st) {
+                  cudaStream_t st, SelectBuckets bk = SelectBuckets{nullptr, nullptr, nullptr, 0}) {
     // 1-D/2-D: one thread per target (k_select_t); dim >= 3: 16-lane groups
     // (windows of many rows)
     constexpr int G = DIM <= 2 ? 8 : 16;
-    k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0);
+    k_stats_init<<<1, 32, 0, st>>>(stats, 8, 0, bk.pos_counts ? bk.bucket_count : nullptr,
+                                   FM_NBUCKETS);
     if (s.nt == 0) return FM_OK;
     if (DIM <= 2 && slot_cap <= 2 * kThreadListCap && !select_groups_forced()) {
         // the per-thread list IS the slot: a position is slotted iff its
@@ -936,10 +963,11 @@ int launch_select(const SearchArgs &s, int32_t min_required, int32_t *counts, do
         const int blocks = (int)std::min<int64_t>((tiles + 3) / 4, (int64_t)kSMs * 8);
         k_select_t<DIM><<<blocks, kBlock, sm, st>>>(s, min_required, lcap, counts, radii, status,
                                                     slot_id, slot_pos, slot_cap, overflow, stats,
-                                                    pos_info, pos_t);
+                                                    pos_info, pos_t, bk);
         FM_CHECK_LAUNCH();
         return FM_OK;
     }
+    if (bk.pos_counts) return FM_ERR_UNSUPPORTED;  // lane-group select: not fused
     const int lcap = slot_cap > kSelectListCap ? slot_cap : kSelectListCap;
     const size_t per = ((size_t)lcap * 16 + sizeof(RowTable<G>) + 15) & ~(size_t)15;
     const size_t sm = per * (kBlock / G);
@@ -1085,7 +1113,7 @@ int launch_fit_many(const fm_fit &fp, const double *targets, int64_t nt, const i
                       double, double *, cudaStream_t);                                            \
     int dim##N##_select(const SearchArgs &, int32_t, int32_t *, double *, uint8_t *, int32_t *,  \
                         int32_t *, int, int32_t *, int32_t *, PosInfo *, double *,            \
-                        cudaStream_t);
+                        cudaStream_t, const SelectBuckets &);
 #define FM_DECLARE_DEG(N, P)                                                                      \
     int dim##N##_deg##P##_build(bool, bool, const SearchArgs &, const BuildArgs &, int,          \
                                 cudaStream_t);                                                    \
@@ -1116,9 +1144,9 @@ FM_DECLARE_DEG(5, 0) FM_DECLARE_DEG(5, 1) FM_DECLARE_DEG(5, 2)
     int dim##N##_select(const SearchArgs &s, int32_t need, int32_t *c, double *r, uint8_t *st,    \
                         int32_t *sid, int32_t *spos, int scap, int32_t *ovf, int32_t *stats,       \
                         PosInfo *pinfo, double *pt,                                                \
-                        cudaStream_t stream) {                                                     \
+                        cudaStream_t stream, const SelectBuckets &bk) {                            \
         return launch_select<N>(s, need, c, r, st, sid, spos, scap, ovf, stats, pinfo, pt,       \
-                                stream);           \
+                                stream, bk);       \
     }
 
 #define FM_DEFINE_DEG(N, P)                                                                        \

@@ -758,7 +758,8 @@ class GraphedTransfer:
         self.stats = e(8 + nb + 2, torch.int32)  # select stats, bucket sizes, fit stats
         self.blist = e(nt * nb, torch.int32)
         self.offsets = e(nt + 1, torch.int64)
-        self.sws_bytes = L.fm_offsets_ordered_workspace(nt)
+        self.pos_counts = e(nt, torch.int32)
+        self.sws_bytes = L.fm_scan_workspace(nt)
         self.sws = _workspace(self.sws_bytes, dev)
         self.col = e(nt * self.cap, torch.int32)
         self.val = e(nt * self.cap, torch.float64)
@@ -786,17 +787,18 @@ class GraphedTransfer:
         main.wait_stream(self._fork)
         csel = self.sel.to_ctypes()
         need = 0 if self.sel.adaptive else _n_monomials(self.dim, self.spec.degree)
-        check(L.fm_select_supports(ctypes.byref(g), ptr(self.cell_start), ptr(self.sorted_pts),
-                                   ptr(self.sorted_ids), ptr(self.tgt), nt, ptr(self.perm),
-                                   ctypes.byref(csel), need, ptr(self.counts), ptr(self.radii),
-                                   ptr(self.status), None, ptr(self.slot_pos), self.cap,
-                                   ptr(self.overflow), ptr(self.stats), ptr(self.pos_info),
-                                   ptr(self.pos_t), st), "fm_select_supports")
-        # row lengths capped at the slot: the offsets stay within nt * cap
-        check(L.fm_offsets_ordered_capped(ptr(self.counts), ptr(self.perm), nt, self.cap, 1,
-                                          ptr(self.offsets), ptr(self.blist),
-                                          ptr(self.stats[8:]), ptr(self.sws), self.sws_bytes,
-                                          st), "fm_offsets_ordered_capped")
+        # the select also writes the row lengths by position (capped: 0 for a
+        # support beyond the slot, so the offsets stay within nt * cap) and
+        # the size buckets; then one scan for the row offsets
+        check(L.fm_select_supports_bucketed(
+            ctypes.byref(g), ptr(self.cell_start), ptr(self.sorted_pts), ptr(self.sorted_ids),
+            ptr(self.tgt), nt, ptr(self.perm), ctypes.byref(csel), need, ptr(self.counts),
+            ptr(self.radii), ptr(self.status), None, ptr(self.slot_pos), self.cap,
+            ptr(self.overflow), ptr(self.stats), ptr(self.pos_info), ptr(self.pos_t), 1,
+            ptr(self.pos_counts), ptr(self.blist), ptr(self.stats[8:]), st),
+            "fm_select_supports_bucketed")
+        check(L.fm_offsets_from_counts(ptr(self.pos_counts), nt, ptr(self.offsets), ptr(self.sws),
+                                       self.sws_bytes, st), "fm_offsets_from_counts")
         nb = _lib.FM_NBUCKETS
         lists = FmLists(self.counts.data_ptr(), None, self.slot_pos.data_ptr(), self.cap, 0,
                         self.overflow.data_ptr(), self.pos_info.data_ptr(),
