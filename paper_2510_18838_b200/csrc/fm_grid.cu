@@ -147,6 +147,7 @@ __global__ void k_place(const int32_t *__restrict__ keys, int64_t n,
             int32_t r = 0;
             for (int32_t k = b; k < e; k++) r += __ldg(arrival + k) < i;
             const int64_t p = b + r;
+            FM_DCHECK(b <= q && q < e && p < e && i >= 0 && i < n);
             ids[p] = i;
 #pragma unroll
             for (int a = 0; a < DIM; a++) sorted_pts[p * DIM + a] = __ldg(pts + (int64_t)i * DIM + a);

@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_select_t(SearchArgs s, int32_t mi
             int at = 0;
             if (lane == leader && b >= 0) at = atomicAdd(bk.bucket_count + b, __popc(peers));
             at = __shfl_sync(FM_FULL_MASK, at, leader);
+            FM_DCHECK(b < 0 || at + __popc(peers) <= s.nt);
             if (b >= 0)
                 bk.bucket_list[(int64_t)b * s.nt + at + __popc(peers & ((1u << lane) - 1u))] =
                     (int32_t)k;
