@@ -47,11 +47,12 @@ __global__ void k_scale_points(const double *__restrict__ pts, int64_t n, int di
 // slower (0.166 ms): the kernel is bound by L1 wavefronts, not by latency;
 // so was (col, val) staged as 16-byte records read with one shared load per
 // nonzero (0.186 ms: 32 KB of staging per block, weights held in registers).
-#ifdef FM_APPLY_MINB
-#define FM_APPLY_BOUNDS __launch_bounds__(256, FM_APPLY_MINB)
-#else
-#define FM_APPLY_BOUNDS __launch_bounds__(256)
+// 4 blocks of 256 per SM = 64 registers (without the minimum, ptxas may
+// settle on 48 and spill)
+#ifndef FM_APPLY_MINB
+#define FM_APPLY_MINB 4
 #endif
+#define FM_APPLY_BOUNDS __launch_bounds__(256, FM_APPLY_MINB)
 template <int L, int V, int CH, bool CS>
 __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict__ row_off,
                                                const int32_t *__restrict__ col,
@@ -82,6 +83,9 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
         const int64_t rb = active ? __ldg(row_off + r) : 0;
         const int64_t re = active ? __ldg(row_off + r + 1) : 0;
         const int64_t tb = __ldg(row_off + r0), te = __ldg(row_off + rend);
+        // the output row's target, loaded now: its latency hides behind the
+        // gathers instead of stalling the store
+        const int64_t t_out = (active && row_target) ? (int64_t)__ldg(row_target + r) : r;
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; v++) acc[v] = 0.0;
@@ -122,8 +126,7 @@ __global__ void FM_APPLY_BOUNDS k_apply(int64_t nrows, const int64_t *__restrict
             __syncwarp();
         }
         if (active) {
-            const int64_t t = row_target ? (int64_t)row_target[r] : r;
-            double *yp = Y + t * C + li * V;
+            double *yp = Y + t_out * C + li * V;
             if (V == 2) {
                 *reinterpret_cast<double2 *>(yp) = make_double2(acc[0], acc[V - 1]);
             } else {
