@@ -761,7 +761,10 @@ class GraphedTransfer:
         self.pos_counts = e(nt, torch.int32)
         self.sws_bytes = L.fm_scan_workspace(nt)
         self.sws = _workspace(self.sws_bytes, dev)
-        self.col = e(nt * self.cap, torch.int32)
+        # zero-filled once: a row the graph does not build (a support in a
+        # size bucket the capture left out, flagged by check()) then holds
+        # in-range column ids -- stale or 0 -- and the apply stays in bounds
+        self.col = torch.zeros(nt * self.cap, dtype=torch.int32, device=dev)
         self.val = e(nt * self.cap, torch.float64)
         self.fstatus = e(nt, torch.uint8)
         edges = _lib.FM_BUCKET_EDGES
@@ -878,6 +881,12 @@ class GraphedTransfer:
             with torch.cuda.stream(side):  # eager pass: lazy attributes/streams outside capture
                 self._launch()
             torch.cuda.current_stream().wait_stream(side)
+            # the graph launches only the size buckets this geometry fills (an
+            # empty bucket's persistent launch still costs its slot in the
+            # step); check() flags a later replay that fills another one
+            counts = self.stats[8:8 + _lib.FM_NBUCKETS].cpu().numpy()
+            used = sum(1 << b for b in range(_lib.FM_NBUCKETS) if counts[b] > 0)
+            self.mask = (self.mask & used) or self.mask
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph):
                 self._launch()
@@ -906,8 +915,10 @@ class GraphedTransfer:
         out = {"max_count": int(h[0]), "short": int(h[2]), "status_fail": int(h[4]),
                "overflow": int(h[6]), "fit_fail": int(h[8 + nb]),
                "buckets": h[8:8 + nb].tolist(), "nnz": int(self.offsets[self.nt].item())}
+        out["unbuilt_bucket"] = any(c > 0 and not (self.mask >> b) & 1
+                                    for b, c in enumerate(out["buckets"]))
         out["valid"] = (out["overflow"] == 0 and out["short"] == 0 and out["status_fail"] == 0
-                        and out["fit_fail"] == 0)
+                        and out["fit_fail"] == 0 and not out["unbuilt_bucket"])
         return out
 
 

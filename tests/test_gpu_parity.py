@@ -1107,3 +1107,33 @@ def test_grid_binning_crowded_and_coincident_cells():
         assert np.array_equal(cloud.cell_start.cpu().numpy(), start), cpp
         assert np.array_equal(cloud.sorted_ids.cpu().numpy(), ids[order]), cpp
         assert np.array_equal(cloud.sorted_pts.cpu().numpy(), src[order]), cpp
+
+
+@pytest.mark.gpu
+def test_graphed_transfer_flags_unbuilt_bucket():
+    """GraphedTransfer captures only the size buckets its first geometry
+    fills; a replay whose supports land in another bucket (same capture key:
+    fixed radius, same sources) must report itself invalid, and a fresh
+    transfer of that input gives the oracle's values."""
+    from paper_2510_18838_b200 import device as D
+    from paper_2510_18838_b200 import pointwise as P
+
+    rs = np.random.RandomState(5)
+    dense = rs.uniform(0.0, 0.5, (2000, 2)) * [1, 2]  # ~2x the density: m ~ 31
+    sparse = rs.uniform(0.5, 1.0, (1000, 2)) * [1, 2]
+    src = np.concatenate([dense, sparse])
+    X = np.stack([np.sin(3 * src[:, 0]), np.cos(2 * src[:, 1])], 1)
+    spec = P.FitSpec(1, P.RadialBasisSpec(P.RbfKind.C4, a=2.0), P.FixedRadius(0.05))
+    t_sparse = rs.uniform(0.6, 0.9, (500, 2)) * [1, 2]
+    t_dense = rs.uniform(0.1, 0.4, (500, 2)) * [1, 2]
+    tgt_d = D.to_device(t_sparse)
+    gt = D.GraphedTransfer(D.to_device(src), tgt_d, D.to_device(X), spec)
+    Y = gt.run()
+    c = gt.check()
+    assert c["valid"], c
+    assert np.allclose(Y.cpu().numpy(), P.fit_point_cloud(src, X, t_sparse, spec), rtol=1e-12,
+                       atol=0)
+    tgt_d.copy_(D.to_device(t_dense))  # ~2x the points per support: other buckets
+    gt.run()
+    c = gt.check()
+    assert c["unbuilt_bucket"] and not c["valid"], c
